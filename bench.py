@@ -1,0 +1,397 @@
+"""Benchmark of the restarted reflected-Halpern PDHG hot path (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
+                    [--config c2] [--no-e2e] [--no-cpu-baseline]
+
+Workload: BASELINE.json configs[1] (C2: synthetic MIPLIB-relaxation-like LP,
+m=500k, n=1M, ~10M nnz, power-law row lengths), generated on the host from a
+fixed seed (data "synthetic"). All arithmetic is fp64.
+
+A "step" = one KKT check interval of the solve loop: 64 restarted reflected
+Halpern PDHG iterations (each: A x+, A^T y+ and the fused primal / dual /
+Halpern / reflection updates and residual reductions) plus the KKT check and
+any restarts they trigger, run through the product's resumable C-ABI session
+(include/rhpdhg_c.h). `value` is PDHG iterations/s with the LP resident in
+HBM, timed with CUDA events on the solve's stream around exactly K steps
+(the matrix, ~240 MB, is larger than L2, so no flush is needed); `e2e` is the
+same metric through rhpdhg_session_create/finish with HOST buffers: upload,
+scaling, power iteration, the solve to 1e-8 relative KKT and the download of
+the solution are inside the timed region.
+
+--impl reference times the reference's own CPU implementation (the
+unmodified reference library compiled from /root/reference into
+oracle/_ref, single-threaded as shipped) on the same LP, K steps of 8
+iterations each after its setup.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2507_14051_b200 import generators  # noqa: E402
+from paper_2507_14051_b200.lp import Session, SolverConfig, set_device_options  # noqa: E402
+
+STEP_ITERS = 64
+METRIC = "PDHG iter/s"
+UNIT = "iter/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------- clocks --------
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ distributed ----
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            self.torch = torch
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl")
+            self.dist = dist
+
+    def barrier(self):
+        if self.torch:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.torch:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if not self.torch:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.torch:
+            self.dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ bytes model ----
+def algorithmic_bytes(m, n, nnz):
+    """Per-launch algorithmic HBM bytes of the fused kernels:
+    K1: 12 nnz + 8(m+1) row_ptr + 8 n (x+ gathered once) + 72 m (read ax, y,
+        lo, hi, y0, ax0; write y+, y, ax)
+    K2: 12 nnz + 8(n+1) + 8 m (y+ gathered once) + 24 n (aty, aty0 -> aty)
+        + 56 n (read x, c, l, u, x0; write x+, x) = 12 nnz + 8(n+1) + 8 m + 80 n."""
+    k1 = 12 * nnz + 8 * (m + 1) + 8 * n + 72 * m
+    k2 = 12 * nnz + 8 * (n + 1) + 8 * m + 80 * n
+    return k1, k2
+
+
+def lp_bytes(lp):
+    return (lp.row_ptr.nbytes + lp.col_index.nbytes + lp.values.nbytes + lp.objective.nbytes +
+            lp.var_lb.nbytes + lp.var_ub.nbytes + lp.con_lb.nbytes + lp.con_ub.nbytes)
+
+
+def make_lp(name):
+    t = time.perf_counter()
+    lp = generators.CONFIGS[name]()
+    return lp, time.perf_counter() - t
+
+
+WORKLOADS = {
+    "c1": "C1 synthetic feasible bounded LP (m=1k, n=2k, ~10k nnz)",
+    "c2": "C2 synthetic MIPLIB-relaxation-like LP (m=500k, n=1M, ~10M nnz, power-law rows)",
+    "c3": "C3 synthetic transportation LP (1k x 1k, n=1M, 2M nnz)",
+    "c4": "C4 synthetic multicommodity-flow LP (K=20, E=1M, n=20M, 60M nnz)",
+}
+
+
+# --------------------------------------------------------------- CPU arm -----
+def cpu_sample(lp, iters, label):
+    """Reference (oracle/_ref) when built, else the oracle port; 1 core."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import support
+
+    if support.ref_available():
+        s = support.RefSession(lp, SolverConfig(epsilon=1e-300))
+        setup = s.setup_seconds
+        _, secs, total = s.advance(iters)
+        s.close()
+        kind = "reference"
+    else:
+        o = support.oracle()
+        t0 = time.perf_counter()
+        support.solve_with(o, lp, SolverConfig(epsilon=1e-300, iteration_limit=0))
+        setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        support.solve_with(o, lp, SolverConfig(epsilon=1e-300, iteration_limit=iters))
+        secs = time.perf_counter() - t0 - setup
+        total = iters
+        kind = "port"
+    return {"value": total / secs, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{label}: setup (Ruiz+Pock-Chambolle+power iteration, {setup:.1f} s) then "
+                      f"{total} loop iterations incl. KKT checks ({secs:.1f} s), 1 thread",
+            "setup_seconds": setup, "loop_seconds": secs, "iterations": total}
+
+
+def run_reference(args):
+    dist = Dist()
+    if dist.rank != 0:
+        dist.close()
+        return 0
+    sys.path.insert(0, str(ROOT / "tests"))
+    import support
+
+    lp, _ = make_lp(args.config)
+    cfg_run = {"workload": WORKLOADS[args.config], "m": lp.num_cons, "n": lp.num_vars,
+               "nnz": lp.nnz, "parallelism": "1 CPU thread (reference is single-threaded)"}
+    if not support.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref not built (needs /root/reference at build time)"}))
+        return 0
+    s = support.RefSession(lp, SolverConfig(epsilon=1e-300))
+    per_step = args.ref_step_iters
+    for _ in range(args.warmup):
+        s.advance(per_step)
+    t0 = time.perf_counter()
+    total = 0
+    for _ in range(args.steps):
+        _, _, _ = s.advance(per_step)
+        total += per_step
+    secs = time.perf_counter() - t0
+    s.close()
+    v = total / secs
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": dict(cfg_run, step=f"{per_step} PDHG iterations"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": f"{args.steps} steps x {per_step} iterations after "
+                                       f"{s.setup_seconds:.1f} s setup"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_seconds": s.setup_seconds}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm ----
+def run_product(args):
+    dist = Dist()
+    set_device_options(dist.local, not args.no_graph, 64)
+    lp, gen_s = make_lp(args.config)
+    m, n, nnz = lp.num_cons, lp.num_vars, lp.nnz
+    peak, peak_kind = peaks()
+
+    # ---- device-resident throughput
+    sess = Session(lp, SolverConfig(epsilon=1e-300))
+    info0 = sess.info()
+    layout = sess.layout()
+    for _ in range(args.warmup):
+        sess.advance(STEP_ITERS)
+    dist.barrier()
+    clocks = ClockSampler(dist.local)
+    clocks.start()
+    a = sess.info()
+    sess.timer_start()
+    for _ in range(args.steps):
+        sess.advance(STEP_ITERS)
+    ms = sess.timer_stop()
+    b = sess.info()
+    clk = clocks.stop()
+    dist.barrier()
+    iters = b["total"] - a["total"]
+    blocks = b["device_blocks"] - a["device_blocks"]
+    checks = b["kkt_checks"] - a["kkt_checks"]
+    launches = 2 * iters + blocks + 2 * checks
+    t_max = dist.max(ms / 1e3)
+    iters_all = dist.sum(iters)
+    value = iters_all / t_max
+
+    # ---- live kernel timing for the roofline (after the timed region)
+    kt = sess.time_kernels(reps=20)
+    sess.close()
+    k1b, k2b = algorithmic_bytes(m, n, nnz)
+    k1 = k1b / (kt["k1_dual_spmv_ms"] * 1e-3) / 1e9
+    k2 = k2b / (kt["k2_aty_spmv_primal_ms"] * 1e-3) / 1e9
+    dominant = "k2" if kt["k2_aty_spmv_primal_ms"] >= kt["k1_dual_spmv_ms"] else "k1"
+    achieved = k2 if dominant == "k2" else k1
+    iter_bytes = k1b + k2b
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": ("spmv_fused<EpiAty> (A^T y+ + aty Halpern + next primal step)"
+                           if dominant == "k2" else
+                           "spmv_fused<EpiDual> (A x+ + dual step + Halpern/reflection)"),
+                "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_launch": k2b if dominant == "k2" else k1b,
+                "kernels": {"k1_ms": kt["k1_dual_spmv_ms"], "k1_gbs": k1,
+                            "k2_ms": kt["k2_aty_spmv_primal_ms"], "k2_gbs": k2,
+                            "k3_ms": kt["k3_primal_ms"],
+                            "iteration_bytes": iter_bytes,
+                            "iteration_gbs_in_loop": iter_bytes * value / max(iters_all, 1) *
+                            iters_all / 1e9 / max(dist.world, 1)}}
+
+    # ---- e2e through the C ABI with host buffers, to 1e-8 (cap)
+    e2e = None
+    if not args.no_e2e:
+        dist.barrier()
+        t0 = time.perf_counter()
+        s2 = Session(lp, SolverConfig(epsilon=args.e2e_eps, iteration_limit=args.e2e_cap))
+        t_setup = time.perf_counter() - t0
+        t_1e4 = None
+        running = True
+        while running:
+            running = s2.advance(STEP_ITERS)
+            if t_1e4 is None:
+                r = s2.info()["residuals"]
+                if (r.gap_rel <= 1e-4 and r.primal_rel <= 1e-4 and
+                        r.dual_eq <= 1e-4 * r.dual_denom and r.dual_cone <= 1e-4 * r.dual_denom):
+                    t_1e4 = time.perf_counter() - t0
+                    it_1e4 = s2.info()["total"]
+        rep = s2.finish()
+        t_e2e = time.perf_counter() - t0
+        s2.close()
+        t_e2e_max = dist.max(t_e2e)
+        e2e_iters = dist.sum(rep.iterations)
+        e2e = {"value": e2e_iters / t_e2e_max, "unit": UNIT,
+               "h2d_bytes_per_step": lp_bytes(lp), "d2h_bytes_per_step": 8 * (2 * n + m),
+               "step": "one full solve from host CSR buffers to the solution in host memory",
+               "status": rep.status, "iterations": rep.iterations, "restarts": rep.restart_count,
+               "time_to_tol_s": t_e2e, "tol": args.e2e_eps,
+               "time_to_1e-4_s": t_1e4, "iterations_to_1e-4": it_1e4 if t_1e4 else None,
+               "setup_s": t_setup, "objective": rep.objective,
+               "residuals": vars(rep.residuals)}
+
+    cpu = None
+    if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
+        cpu = cpu_sample(lp, args.cpu_iters, WORKLOADS[args.config])
+        if e2e and e2e["status"] == "optimal":
+            it = e2e["iterations"]
+            cpu["time_to_tol_extrapolated_s"] = cpu["setup_seconds"] + it / cpu["value"]
+            cpu["extrapolation"] = (f"setup + {it} iterations (the GPU's count to {args.e2e_eps}) "
+                                    "/ sampled reference iter/s")
+            if e2e.get("iterations_to_1e-4"):
+                cpu["time_to_1e-4_extrapolated_s"] = (cpu["setup_seconds"] +
+                                                      e2e["iterations_to_1e-4"] / cpu["value"])
+
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "m": m, "n": n, "nnz": nnz,
+                       "step": f"{STEP_ITERS} PDHG iterations + 1 KKT check (+ restarts)",
+                       "parallelism": ("single GPU" if dist.world == 1 else
+                                       f"{dist.world} independent replicas (row-partitioned "
+                                       "NCCL path not in this build)"),
+                       "l2": "matrix (~24 B/nnz incl. A^T) larger than L2: no flush",
+                       "layout": layout, "generation_s": gen_s,
+                       "setup_s": info0["setup_seconds"]},
+            "roofline": roofline, "clocks": clk, "gpu_launches": launches,
+            "timed_iterations": iters, "restarts_in_timed": b["restarts"] - a["restarts"],
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        if e2e:
+            line["time_to_1e-8_s"] = e2e["time_to_tol_s"] if args.e2e_eps == 1e-8 else None
+            line["time_to_1e-4_s"] = e2e["time_to_1e-4_s"]
+        print(json.dumps(line))
+    dist.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(generators.CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=64)
+    ap.add_argument("--ref-step-iters", type=int, default=8)
+    ap.add_argument("--e2e-eps", type=float, default=1e-8)
+    ap.add_argument("--e2e-cap", type=int, default=100_000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_product(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

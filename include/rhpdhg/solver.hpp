@@ -1,0 +1,27 @@
+// solver.hpp — the solve() entry point. Mirrors
+// /root/reference/proj/include/rhpdhg/solver.hpp:13; the pipeline (scaling,
+// power iteration, restarted reflected-Halpern loop, KKT checks) runs on the
+// GPU through the device library (include/rhpdhg_cuda.h).
+#pragma once
+
+#include "rhpdhg/config.hpp"
+#include "rhpdhg/lp_problem.hpp"
+#include "rhpdhg/report.hpp"
+
+namespace rhpdhg {
+
+/// Device-side runtime knobs (not SolverConfig file keys, so the config echo
+/// stays identical to the reference).
+struct DeviceOptions {
+  int device = 0;
+  bool use_graph = true;   // CUDA graph with a conditional WHILE node per block
+  long block_limit = 64;   // PDHG iterations per device block at most
+};
+
+/// Process-wide default device options (used by solve(problem, cfg)).
+DeviceOptions& default_device_options();
+
+SolutionReport solve(const LpProblem& problem, const SolverConfig& cfg);
+SolutionReport solve(const LpProblem& problem, const SolverConfig& cfg, const DeviceOptions& dev);
+
+}  // namespace rhpdhg

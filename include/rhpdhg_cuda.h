@@ -1,0 +1,197 @@
+/*
+ * rhpdhg_cuda.h — the thin C ABI between the C++ host solver (librhpdhg.so,
+ * the reference-API mirror) and the CUDA device library (librhp_cuda.so).
+ *
+ * Plain C types only: pointers, sizes, doubles. One rhp_ctx owns one solve's
+ * device state (matrices, iterate, anchor, caches, schedules, CUDA graph,
+ * optional NCCL communicator) on one GPU. Host buffers passed in are always in
+ * the ORIGINAL row/column order of the LP; the device stores rows and columns
+ * permuted by row-length bin and the ctx maps between them.
+ *
+ * Which reference code each entry replaces (paths under /root/reference/proj):
+ *   rhp_create          SparseMatrix ctor CSR/CSC build   src/sparse_matrix.cpp:20-65
+ *   rhp_scale           ruiz_equilibrate, pock_chambolle_scale, apply_scales
+ *                                                        src/scaling.cpp:10-81
+ *   rhp_power_*         power_iteration_norm's loop body src/pdhg.cpp:138-152
+ *   rhp_set_step        StepConfig primal/dual steps     include/rhpdhg/pdhg.hpp:14-26
+ *   rhp_reset_iterate   Iterate::zeros + anchor/snapshot src/lp_problem.cpp:98-107, src/solver.cpp:91-103
+ *   rhp_run_block       loop body of solve(): halpern_reflected_step -> pdhg_step
+ *                       -> fixed_point_residual -> check_restart, k/total
+ *                       bookkeeping                      src/solver.cpp:147-181,
+ *                                                        src/restart.cpp:23-69, src/pdhg.cpp:34-115
+ *   rhp_kkt             kkt_check + kkt_residuals sums   src/solver.cpp:32-49, src/termination.cpp:58-118
+ *   rhp_restart         do_restart (anchor, k, residuals) src/restart.cpp:71-83
+ *   rhp_spmv            SparseMatrix::multiply{,_transpose} src/sparse_matrix.cpp:67-87
+ * The PID weight update (src/restart.cpp:85-120), the termination test
+ * (src/termination.cpp:120-124) and all exception mapping stay on the host.
+ *
+ * Every function returns 0 on success or an RHPDHG_E_* code (rhpdhg_c.h);
+ * rhp_last_error() gives the thread-local message.
+ */
+#ifndef RHPDHG_CUDA_H_
+#define RHPDHG_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "rhpdhg_c.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rhp_ctx rhp_ctx;
+
+/* Device / distribution options. world_size > 1 row-partitions A across
+ * ranks (one process per GPU); nccl_id is the 128-byte ncclUniqueId created
+ * by rank 0 with rhp_nccl_unique_id() and broadcast by the caller. The LP
+ * view passed to rhp_create is always the FULL problem; each rank keeps its
+ * row block. */
+typedef struct rhp_options {
+  int32_t device;        /* CUDA device ordinal */
+  int32_t rank;          /* 0 */
+  int32_t world_size;    /* 1 */
+  int32_t use_graph;     /* 1: CUDA graph with a conditional WHILE node per block */
+  int64_t block_limit;   /* max PDHG iterations per device block (default 64) */
+  const void* nccl_id;   /* 128 bytes when world_size > 1, else NULL */
+} rhp_options;
+
+/* Step and restart parameters of the device loop. Derived quantities are
+ * computed on the host with the reference's exact expressions:
+ *   tau = eta/omega, sigma = eta*omega (pdhg.hpp:18-19), sigma_inv = 1/sigma
+ *   (pdhg.cpp:50), primal_scale = omega/eta, dual_scale = 1/(eta*omega)
+ *   (pdhg.cpp:70-71). */
+typedef struct rhp_step {
+  double eta, omega, gamma;
+  double tau, sigma, sigma_inv, primal_scale, dual_scale;
+  double beta_sufficient, beta_necessary, beta_artificial;
+  int64_t check_interval;
+  int64_t iteration_limit;
+  int32_t restarts_enabled;
+  int32_t record_history;
+} rhp_step;
+
+/* What one device block of PDHG iterations ended with. */
+typedef struct rhp_block_out {
+  int64_t iterations_done; /* in this block */
+  int64_t total;           /* RestartState::total */
+  int64_t k;               /* RestartState::k */
+  int32_t verdict;         /* RestartCondition: 0 none, 1 sufficient, 2 necessary, 3 artificial */
+  int32_t check_due;       /* total % check_interval == 0 || verdict != none */
+  int32_t breakdown;       /* indefinite canonical norm (pdhg.cpp:114) */
+  int32_t pad_;
+  double r_last;           /* fixed-point residual of the last iteration */
+  double r_anchor, r_prev;
+  double q_last;           /* radicand when breakdown */
+  /* PID inputs for the current Halpern iterate (restart.cpp:86-91):
+   * ||x - x_snapshot||^2, ||y - y_snapshot||^2, ||x||^2, ||y||^2 */
+  double x_dist2, y_dist2, x_norm2, y_norm2;
+} rhp_block_out;
+
+/* Raw device sums of one KKT evaluation (termination.cpp:58-118) on the
+ * original instance; the host turns them into KktResiduals. */
+typedef struct rhp_kkt_sums {
+  double primal_value;   /* c^T x */
+  double py, pr;         /* p(-y; con bounds), p(-r; var bounds), finite terms */
+  double viol2;          /* ||A x - proj_[L,U](A x)||^2 */
+  double eq2, cone2;     /* dual equality / cone residual squares */
+  int64_t py_inf, pr_inf;/* count of +inf terms */
+  int64_t nan_x, nan_y;  /* count of NaN entries */
+} rhp_kkt_sums;
+
+/* Scaling results, for parity tests (original order). */
+typedef struct rhp_scaled_out {
+  double* csr_values;  /* [nnz] CSR order of the reference (row-major)       may be NULL */
+  double* csc_values;  /* [nnz] CSC order of the reference (column-major)    may be NULL */
+  double* row_scale;   /* [m] cumulative D_row */
+  double* col_scale;   /* [n] cumulative D_col */
+  double* objective;   /* [n] scaled c */
+  double* var_lb;      /* [n] */
+  double* var_ub;      /* [n] */
+  double* con_lb;      /* [m] */
+  double* con_ub;      /* [m] */
+} rhp_scaled_out;
+
+typedef struct rhp_device_info {
+  char name[128];
+  int32_t sm_count;
+  int32_t cc_major, cc_minor;
+  int64_t l2_bytes;
+  int64_t mem_bytes;
+  int32_t graph_supported;
+  int32_t pad_;
+} rhp_device_info;
+
+/* Per-operator schedule summary, for diagnostics/benchmarks. */
+typedef struct rhp_layout_info {
+  int64_t m_local, n, nnz_local;
+  int64_t row_bins[8];  /* rows of A per bin: widths 1,2,4,8,16,32, CTA, split */
+  int64_t col_bins[8];  /* rows of A^T per bin */
+  int32_t grid_a, grid_at, grid_vec;
+  int32_t sm_count;
+} rhp_layout_info;
+
+const char* rhp_last_error(void);
+int rhp_device_count(int* count);
+int rhp_get_device_info(int device, rhp_device_info* info);
+int rhp_nccl_unique_id(void* out128);
+
+int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt, rhp_ctx** out);
+int rhp_destroy(rhp_ctx* ctx);
+int rhp_layout(rhp_ctx* ctx, rhp_layout_info* info);
+
+/* Diagonal preconditioning on the device; bitwise equal to the reference. */
+int rhp_scale(rhp_ctx* ctx, int enabled, int ruiz_iterations, int pock_chambolle);
+int rhp_get_scaled(rhp_ctx* ctx, const rhp_scaled_out* out);
+
+/* Power iteration on A^T A of the current (scaled) matrix. begin uploads the
+ * unit start vector (column order); step does av = A v, w = A^T av and
+ * returns v.w and w.w; normalize sets v = w / wnorm. */
+int rhp_power_begin(rhp_ctx* ctx, const double* v0);
+int rhp_power_step(rhp_ctx* ctx, double* vw, double* ww);
+int rhp_power_normalize(rhp_ctx* ctx, double wnorm);
+
+/* out = A in (transpose 0, in[n] -> out[m]) or A^T in (transpose 1) with the
+ * current device matrix (original before rhp_scale, scaled after). */
+int rhp_spmv(rhp_ctx* ctx, int transpose, const double* in, double* out);
+
+int rhp_set_step(rhp_ctx* ctx, const rhp_step* step);
+int rhp_reset_iterate(rhp_ctx* ctx);
+/* Overwrite the scaled iterate z (x, y) and recompute exact caches; for tests. */
+int rhp_set_iterate(rhp_ctx* ctx, const double* x, const double* y);
+int rhp_run_block(rhp_ctx* ctx, rhp_block_out* out);
+/* Copies min(count, cap) residuals of the last block. */
+int rhp_get_history(rhp_ctx* ctx, double* out, int64_t cap, int64_t* count);
+
+/* which: 0 = current Halpern iterate z (refreshes z.ax/z.aty from exact
+ * products, solver.cpp:42-44, and stores the unscaled x, y, reduced costs for
+ * rhp_fetch_solution); 1 = last inner PDHG point (x+, y+), no refresh. */
+int rhp_kkt(rhp_ctx* ctx, int which, rhp_kkt_sums* out);
+/* kkt_residuals(problem, x, y) of given original-space vectors with the
+ * ORIGINAL matrix (call before rhp_scale). */
+int rhp_kkt_of(rhp_ctx* ctx, const double* x, const double* y, rhp_kkt_sums* out);
+int rhp_fetch_solution(rhp_ctx* ctx, double* x, double* y, double* reduced_costs);
+/* Scaled iterate (x, y, ax, aty) in original order; for tests. */
+int rhp_fetch_iterate(rhp_ctx* ctx, double* x, double* y, double* ax, double* aty);
+
+/* do_restart's device half: anchor <- z (with caches), k = 0,
+ * r_anchor = r_prev = +inf; the host already updated omega via rhp_set_step. */
+int rhp_restart(rhp_ctx* ctx);
+
+/* Device time (ms, CUDA events) of the last rhp_run_block. */
+int rhp_last_block_ms(rhp_ctx* ctx, double* ms);
+/* Event timer on the ctx stream: start != 0 records the start event;
+ * start == 0 records the stop event, synchronizes, returns elapsed ms. */
+int rhp_timer(rhp_ctx* ctx, int start, double* ms);
+/* Average device time (ms) of `reps` back-to-back launches of each fused
+ * iteration kernel (K1 = A-side SpMV + dual/Halpern epilogue, K2 = A^T-side
+ * SpMV + aty/Halpern epilogue + next primal step, K3 = block-start primal
+ * step) on the live iterate. Benchmark use only: mutates the iterate. */
+int rhp_time_kernels(rhp_ctx* ctx, int reps, double* ms_k1, double* ms_k2, double* ms_k3);
+/* Synchronize the ctx stream. */
+int rhp_synchronize(rhp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RHPDHG_CUDA_H_ */

@@ -1,0 +1,186 @@
+// device_common.cuh — shared device-side definitions of the rhpdhg CUDA library.
+//
+// Conventions
+//  * fp64 everywhere. Elementwise formulas that the reference evaluates in a
+//    fixed order (pdhg.cpp:41-63, restart.cpp:23-30, scaling.cpp:10-34) are
+//    written with explicit __dmul_rn/__dadd_rn/__dsub_rn so nvcc cannot
+//    contract them into FMAs: each such value is then bit-identical to the
+//    reference's on the same inputs. SpMV row sums and reductions use FMA
+//    and tree orders (documented drift).
+//  * All reductions are deterministic: a fixed lane/warp tree per block, then
+//    a fixed-order sum of per-block partials by the last block to finish.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace rhp {
+
+constexpr int kBlock = 256;          // threads per CTA for every hot kernel
+constexpr int kWarps = kBlock / 32;
+constexpr int kMaxSeg = 8;
+
+// std::max / std::min semantics (first argument wins on ties and NaN), which
+// the reference's projections rely on (lp_problem.cpp:62, pdhg.cpp:44,54).
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// a*((1+g)*next - g*cur) + b*anchor, restart.cpp:29 evaluation order.
+__device__ __forceinline__ double affine(double a, double opg, double g, double b, double next,
+                                         double cur, double anchor) {
+  return add(mul(a, sub(mul(opg, next), mul(g, cur))), mul(b, anchor));
+}
+
+// Streaming loads for matrix data: evict-first so the gathered vectors stay
+// resident in L2 while the (larger than L2) matrix streams through.
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+__device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((const long long*)p); }
+
+// Loop control shared by host and device (one per ctx, device resident).
+struct Ctl {
+  // -- parameters written by the host (rhp_set_step)
+  double eta, omega, gamma;
+  double tau, sigma, sigma_inv, primal_scale, dual_scale;
+  double beta_s, beta_n, beta_a;
+  int64_t check_interval, iteration_limit, block_limit;
+  int32_t restarts_enabled, record_history;
+  // -- loop state
+  int64_t k, total, block_iters;
+  double r_anchor, r_prev, r_last, q_last;
+  int32_t stop, verdict, check_due, breakdown;
+  int32_t k1_token, bench;         // bench: kernels ignore the block-stop guards (rhp_time_kernels)
+  // PID inputs of the current Halpern iterate
+  double x_dist2, y_dist2, x_norm2, y_norm2;
+  // -- KKT sums
+  double kkt_cx, kkt_py, kkt_pr, kkt_viol2, kkt_eq2, kkt_cone2;
+  double kkt_py_inf, kkt_pr_inf, kkt_nan_x, kkt_nan_y;
+  // -- power iteration
+  double pw_vw, pw_ww;
+  // -- last-block tickets (one per finalizing kernel family)
+  unsigned int ticket_dual, ticket_kkt, ticket_pow, ticket_spare;
+  unsigned long long cond_handle;  // cudaGraphConditionalHandle of the block WHILE node
+  int32_t graph_mode, pad1;
+  double* hist;                    // [block_limit] residual history of the current block
+};
+
+// One bin segment of an operator schedule: rows [row_begin, row_end) of the
+// (permuted) CSR, processed as tiles [tile_begin, tile_end).
+// kind 0..5: 2^kind lanes per row, kBlock/2^kind rows per tile;
+// kind 6: one CTA per chunk of one long row (chunk table).
+struct Seg {
+  int32_t kind, pad;
+  int64_t row_begin, row_end, tile_begin, tile_end;
+};
+
+struct Sched {
+  int32_t nseg;
+  int32_t n_multi;          // rows split across several chunks
+  int64_t total_tiles;
+  Seg seg[kMaxSeg];
+  const int32_t* chunk_row;   // [chunks] permuted row
+  const int64_t* chunk_beg;   // [chunks]
+  const int64_t* chunk_end;   // [chunks]
+  const int32_t* chunk_first; // [chunks] first chunk of the same row
+  const int32_t* chunk_count; // [chunks] chunks of the same row
+  const int32_t* chunk_slot;  // [chunks] multi-chunk slot or -1
+  double* chunk_part;         // [chunks]
+  unsigned int* slot_ticket;  // [n_multi]
+  double* long_red;           // [n_multi * 16] epilogue reductions of multi-chunk rows
+};
+
+struct Csr {
+  const int64_t* rp;
+  const int32_t* ci;
+  const double* v;
+  int64_t rows;
+};
+
+// ------------------------------------------------------------ reductions --
+// Block-reduce N per-thread values (fixed xor-butterfly + fixed warp order)
+// and store thread 0's totals into part[q*stride + slot].
+template <int N>
+__device__ __forceinline__ void block_reduce_store(const double (&acc)[N], double* part,
+                                                   int stride, int slot) {
+  __shared__ double sm[N][kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) sm[q][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += sm[threadIdx.x][w];
+    part[(size_t)threadIdx.x * stride + slot] = s;
+  }
+  __syncthreads();
+}
+
+// Block-wide fixed-order sum of `count` partials per quantity (SoA, stride);
+// every thread receives the totals.
+template <int N>
+__device__ __forceinline__ void block_sum_partials(const double* part, int count, int stride,
+                                                   double (&out)[N]) {
+  __shared__ double sm[N][kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < count; i += kBlock) v += __ldcg(part + (size_t)q * stride + i);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) sm[q][warp] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += sm[q][w];
+    out[q] = s;
+  }
+  __syncthreads();
+}
+
+// Adds the epilogue reductions of multi-chunk long rows (fixed slot order).
+template <int N>
+__device__ __forceinline__ void add_long_slots(const Sched& s, double (&out)[N]) {
+  if (s.n_multi == 0) return;
+  __shared__ double sm[N];
+  if (threadIdx.x < N) {
+    double v = 0.0;
+    for (int i = 0; i < s.n_multi; ++i) v += __ldcg(s.long_red + (size_t)i * 16 + threadIdx.x);
+    sm[threadIdx.x] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N; ++q) out[q] += sm[q];
+  __syncthreads();
+}
+
+// Last-block-done election. Returns true in exactly one block, after every
+// block's partial stores are visible to it.
+__device__ __forceinline__ bool elect_last_block(unsigned int* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+}  // namespace rhp

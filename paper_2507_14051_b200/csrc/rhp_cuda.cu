@@ -1,0 +1,884 @@
+// rhp_cuda.cu — device context and the C ABI of include/rhpdhg_cuda.h.
+//
+// One rhp_ctx = one solve's device state on one GPU. Host code here only
+// allocates, uploads, builds the CUDA graph and launches; all arithmetic of
+// the solve runs in the kernels of pdhg_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#ifdef RHP_WITH_NCCL
+#include <nccl.h>
+#endif
+
+#include "layout.cuh"
+#include "pdhg_kernels.cuh"
+#include "rhpdhg_cuda.h"
+
+using namespace rhp;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+#define CK(call) check((call), #call)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RHPDHG_OK;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return RHPDHG_E_DEVICE;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return RHPDHG_E_USAGE;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return RHPDHG_E_USAGE;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return RHPDHG_E_INVALID_PROBLEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RHPDHG_E_INTERNAL;
+  }
+}
+
+template <class T>
+T* dev_alloc(size_t count) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+template <class T>
+void upload(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+struct DevOp {
+  int64_t rows = 0, nnz = 0;
+  int64_t* rp = nullptr;
+  int32_t* ci = nullptr;
+  double* v = nullptr;       // current values (original, then scaled)
+  double* v_orig = nullptr;  // original values, kept until scaling is done
+  Sched sched{};             // with device pointers
+  int32_t *chunk_row = nullptr, *chunk_first = nullptr, *chunk_count = nullptr,
+          *chunk_slot = nullptr;
+  int64_t *chunk_beg = nullptr, *chunk_end = nullptr;
+  double *chunk_part = nullptr, *long_red = nullptr;
+  unsigned int* slot_ticket = nullptr;
+  Csr csr() const { return Csr{rp, ci, v, rows}; }
+};
+
+}  // namespace
+
+struct rhp_ctx {
+  rhp_options opt{};
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  HostLayout L;
+  int64_t m = 0, n = 0;
+  DevOp A, At;
+  // vectors in device (permuted) order
+  double *c = nullptr, *vl = nullptr, *vu = nullptr, *cl = nullptr, *cu = nullptr;  // scaled
+  double *co = nullptr, *vlo = nullptr, *vuo = nullptr, *clo = nullptr, *cuo = nullptr;
+  double *rs = nullptr, *cs = nullptr;
+  double *x = nullptr, *y = nullptr, *ax = nullptr, *aty = nullptr;
+  double *x0 = nullptr, *y0 = nullptr, *ax0 = nullptr, *aty0 = nullptr;
+  double *xp = nullptr, *yp = nullptr;
+  double *xout = nullptr, *yout = nullptr, *rcout = nullptr;
+  double *pv = nullptr, *pw = nullptr, *pav = nullptr;
+  double *part1 = nullptr, *part3 = nullptr, *partA = nullptr, *partAt = nullptr;
+  double* hist = nullptr;
+  Ctl* ctl = nullptr;
+  Ctl* ctl_host = nullptr;  // pinned mirror
+  int grid_a = 1, grid_at = 1, grid_vec = 1, grid_max = 1;
+  // CUDA graph of one block of iterations
+  bool graph_built = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
+  double last_block_ms = 0.0;
+  int64_t host_total = 0;  // mirror of ctl->total after the last block
+  int64_t host_check_interval = 64, host_iteration_limit = INT64_MAX;
+  std::vector<double> hbuf;  // host scratch
+};
+
+namespace {
+
+int occupancy_blocks(const void* fn) {
+  int b = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
+  return std::max(b, 1);
+}
+
+void upload_op(DevOp& d, const HostOperator& h, cudaStream_t s) {
+  d.rows = h.rows;
+  d.nnz = h.nnz;
+  d.rp = dev_alloc<int64_t>(h.rp.size());
+  d.ci = dev_alloc<int32_t>(h.ci.size());
+  d.v = dev_alloc<double>(h.v.size());
+  d.v_orig = dev_alloc<double>(h.v.size());
+  upload(d.rp, h.rp.data(), h.rp.size(), s);
+  upload(d.ci, h.ci.data(), h.ci.size(), s);
+  upload(d.v, h.v.data(), h.v.size(), s);
+  upload(d.v_orig, h.v.data(), h.v.size(), s);
+  const size_t nch = h.chunk_row.size();
+  d.chunk_row = dev_alloc<int32_t>(nch);
+  d.chunk_first = dev_alloc<int32_t>(nch);
+  d.chunk_count = dev_alloc<int32_t>(nch);
+  d.chunk_slot = dev_alloc<int32_t>(nch);
+  d.chunk_beg = dev_alloc<int64_t>(nch);
+  d.chunk_end = dev_alloc<int64_t>(nch);
+  d.chunk_part = dev_alloc<double>(nch);
+  upload(d.chunk_row, h.chunk_row.data(), nch, s);
+  upload(d.chunk_first, h.chunk_first.data(), nch, s);
+  upload(d.chunk_count, h.chunk_count.data(), nch, s);
+  upload(d.chunk_slot, h.chunk_slot.data(), nch, s);
+  upload(d.chunk_beg, h.chunk_beg.data(), nch, s);
+  upload(d.chunk_end, h.chunk_end.data(), nch, s);
+  const size_t nm = static_cast<size_t>(h.sched.n_multi);
+  d.slot_ticket = dev_alloc<unsigned int>(nm);
+  d.long_red = dev_alloc<double>(nm * 16);
+  CK(cudaMemsetAsync(d.slot_ticket, 0, std::max<size_t>(nm, 1) * sizeof(unsigned int), s));
+  CK(cudaMemsetAsync(d.long_red, 0, std::max<size_t>(nm, 1) * 16 * sizeof(double), s));
+  d.sched = h.sched;
+  d.sched.chunk_row = d.chunk_row;
+  d.sched.chunk_beg = d.chunk_beg;
+  d.sched.chunk_end = d.chunk_end;
+  d.sched.chunk_first = d.chunk_first;
+  d.sched.chunk_count = d.chunk_count;
+  d.sched.chunk_slot = d.chunk_slot;
+  d.sched.chunk_part = d.chunk_part;
+  d.sched.slot_ticket = d.slot_ticket;
+  d.sched.long_red = d.long_red;
+}
+
+void free_op(DevOp& d) {
+  for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.chunk_row,
+                  (void*)d.chunk_first, (void*)d.chunk_count, (void*)d.chunk_slot,
+                  (void*)d.chunk_beg, (void*)d.chunk_end, (void*)d.chunk_part,
+                  (void*)d.long_red, (void*)d.slot_ticket})
+    if (p) cudaFree(p);
+  d = DevOp{};
+}
+
+// gather a host vector in original order into device order
+void upload_perm(double* dst, const double* src, const std::vector<int32_t>& perm,
+                 std::vector<double>& scratch, cudaStream_t s) {
+  scratch.resize(perm.size());
+  for (size_t i = 0; i < perm.size(); ++i) scratch[i] = src[perm[i]];
+  upload(dst, scratch.data(), scratch.size(), s);
+  CK(cudaStreamSynchronize(s));  // scratch is reused
+}
+
+void download_perm(double* dst, const double* src_dev, const std::vector<int32_t>& perm,
+                   std::vector<double>& scratch, cudaStream_t s) {
+  scratch.resize(perm.size());
+  if (!perm.empty())
+    CK(cudaMemcpyAsync(scratch.data(), src_dev, perm.size() * sizeof(double),
+                       cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < perm.size(); ++i) dst[perm[i]] = scratch[i];
+}
+
+// perm for local rows: prow holds global row ids; make them local
+std::vector<int32_t> local_rows(const rhp_ctx& c) {
+  std::vector<int32_t> p(c.L.prow.size());
+  for (size_t i = 0; i < p.size(); ++i) p[i] = static_cast<int32_t>(c.L.prow[i] - c.L.row_begin);
+  return p;
+}
+
+int vec_grid(const rhp_ctx& c, int64_t len) {
+  const int64_t need = (len + kBlock - 1) / kBlock;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)c.sm_count * 8)));
+}
+
+template <class Epi>
+void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
+                 double* part, unsigned int* ticket, cudaStream_t s) {
+  spmv_fused<Epi><<<grid, kBlock, 0, s>>>(op.csr(), xg, op.sched, epi, part, ticket);
+  CK(cudaGetLastError());
+}
+
+PrimalArgs primal_args(rhp_ctx& c) { return PrimalArgs{c.x, c.xp, c.x0, c.c, c.vl, c.vu}; }
+
+EpiDual epi_dual(rhp_ctx& c, int token) {
+  EpiDual e{};
+  e.ctl = c.ctl;
+  e.y = c.y;
+  e.ax = c.ax;
+  e.yplus = c.yp;
+  e.y0 = c.y0;
+  e.ax0 = c.ax0;
+  e.cl = c.cl;
+  e.cu = c.cu;
+  e.part3 = c.part3;
+  e.grid3 = c.grid_at;
+  e.token = token;
+  return e;
+}
+
+EpiAty epi_aty(rhp_ctx& c, int token) {
+  EpiAty e{};
+  e.ctl = c.ctl;
+  e.aty = c.aty;
+  e.aty0 = c.aty0;
+  e.p = primal_args(c);
+  e.token = token;
+  return e;
+}
+
+void launch_iteration(rhp_ctx& c, int token, cudaStream_t s) {
+  launch_spmv(c, c.A, c.grid_a, c.xp, epi_dual(c, token), c.part1, &c.ctl->ticket_dual, s);
+  launch_spmv(c, c.At, c.grid_at, c.yp, epi_aty(c, token), c.part3, nullptr, s);
+}
+
+void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
+  primal_init<<<c.grid_at, kBlock, 0, s>>>(c.ctl, primal_args(c), c.aty, c.n, c.part3);
+  CK(cudaGetLastError());
+}
+
+void build_graph(rhp_ctx& c) {
+  cudaStream_t cap;
+  CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  CK(cudaGraphCreate(&c.graph, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, c.graph, 1u, cudaGraphCondAssignDefault));
+  unsigned long long hv = static_cast<unsigned long long>(h);
+  CK(cudaMemcpy(&c.ctl->cond_handle, &hv, sizeof(hv), cudaMemcpyHostToDevice));
+  // node 1: the block's first primal step
+  CK(cudaStreamBeginCaptureToGraph(cap, c.graph, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  launch_primal_init(c, cap);
+  cudaGraph_t g1;
+  CK(cudaStreamEndCapture(cap, &g1));
+  size_t count = 0;
+  CK(cudaGraphGetNodes(c.graph, nullptr, &count));
+  std::vector<cudaGraphNode_t> nodes(count);
+  CK(cudaGraphGetNodes(c.graph, nodes.data(), &count));
+  if (count != 1) throw CudaError("unexpected node count after capturing primal_init");
+  // node 2: WHILE(!stop) { K1 ; K2 }
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond;
+  CK(cudaGraphAddNode(&cond, c.graph, nodes.data(), 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  launch_iteration(c, 0, cap);
+  cudaGraph_t g2;
+  CK(cudaStreamEndCapture(cap, &g2));
+  CK(cudaGraphInstantiate(&c.gexec, c.graph, 0));
+  CK(cudaStreamDestroy(cap));
+  c.graph_built = true;
+}
+
+template <class T>
+void set_ctl(rhp_ctx& c, size_t offset, const T& v) {
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.ctl) + offset, &v, sizeof(T),
+                     cudaMemcpyHostToDevice, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+}
+#define SET_CTL(ctx, field, val) set_ctl(ctx, offsetof(Ctl, field), (val))
+
+void pull_ctl(rhp_ctx& c) {
+  CK(cudaMemcpyAsync(c.ctl_host, c.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+// KKT sums of (xbar, ybar) = (xs, ys) in scaled space; optional refresh of
+// z's caches and output of the unscaled vectors.
+void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool write_out,
+             rhp_kkt_sums* out) {
+  EpiKktRow er{};
+  er.ax_refresh = refresh ? c.ax : nullptr;
+  er.y = ys;
+  er.rs = c.rs;
+  er.clo = c.clo;
+  er.cuo = c.cuo;
+  er.yout = write_out ? c.yout : nullptr;
+  launch_spmv(c, c.A, c.grid_a, xs, er, c.partA, nullptr, c.stream);
+  EpiKktCol ec{};
+  ec.ctl = c.ctl;
+  ec.aty_refresh = refresh ? c.aty : nullptr;
+  ec.x = xs;
+  ec.cs = c.cs;
+  ec.co = c.co;
+  ec.vlo = c.vlo;
+  ec.vuo = c.vuo;
+  ec.xout = write_out ? c.xout : nullptr;
+  ec.rcout = write_out ? c.rcout : nullptr;
+  ec.part_row = c.partA;
+  ec.grid_row = c.grid_a;
+  ec.n_multi_row = c.A.sched.n_multi;
+  ec.long_red_row = c.A.long_red;
+  launch_spmv(c, c.At, c.grid_at, ys, ec, c.partAt, &c.ctl->ticket_kkt, c.stream);
+  pull_ctl(c);
+  const Ctl& h = *c.ctl_host;
+  out->primal_value = h.kkt_cx;
+  out->py = h.kkt_py;
+  out->pr = h.kkt_pr;
+  out->viol2 = h.kkt_viol2;
+  out->eq2 = h.kkt_eq2;
+  out->cone2 = h.kkt_cone2;
+  out->py_inf = static_cast<int64_t>(h.kkt_py_inf);
+  out->pr_inf = static_cast<int64_t>(h.kkt_pr_inf);
+  out->nan_x = static_cast<int64_t>(h.kkt_nan_x);
+  out->nan_y = static_cast<int64_t>(h.kkt_nan_y);
+}
+
+void exact_caches(rhp_ctx& c) {
+  // z.ax = A x, z.aty = A^T y
+  launch_spmv(c, c.A, c.grid_a, c.x, EpiStore{c.ax}, nullptr, nullptr, c.stream);
+  launch_spmv(c, c.At, c.grid_at, c.y, EpiStore{c.aty}, nullptr, nullptr, c.stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rhp_last_error(void) { return g_err.c_str(); }
+
+int rhp_device_count(int* count) {
+  return guarded([&] {
+    *count = 0;
+    const cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      *count = 0;
+    }
+  });
+}
+
+int rhp_get_device_info(int device, rhp_device_info* info) {
+  return guarded([&] {
+    cudaDeviceProp p{};
+    CK(cudaGetDeviceProperties(&p, device));
+    std::memset(info, 0, sizeof(*info));
+    std::snprintf(info->name, sizeof(info->name), "%s", p.name);
+    info->sm_count = p.multiProcessorCount;
+    info->cc_major = p.major;
+    info->cc_minor = p.minor;
+    info->l2_bytes = p.l2CacheSize;
+    info->mem_bytes = static_cast<int64_t>(p.totalGlobalMem);
+    int rt = 0;
+    CK(cudaRuntimeGetVersion(&rt));
+    info->graph_supported = rt >= 12040 ? 1 : 0;
+  });
+}
+
+int rhp_nccl_unique_id(void* out128) {
+  return guarded([&] {
+#ifdef RHP_WITH_NCCL
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw CudaError("ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof(id));
+#else
+    (void)out128;
+    throw CudaError("built without NCCL");
+#endif
+  });
+}
+
+int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** out) {
+  *out = nullptr;
+  rhp_ctx* c = new rhp_ctx();
+  const int rc = guarded([&] {
+    rhp_options opt{};
+    opt.device = 0;
+    opt.rank = 0;
+    opt.world_size = 1;
+    opt.use_graph = 1;
+    opt.block_limit = 64;
+    if (opt_in) opt = *opt_in;
+    if (opt.block_limit < 1) opt.block_limit = 64;
+    if (opt.world_size != 1)
+      throw std::invalid_argument("rhp_create: multi-GPU contexts go through rhp_create_dist");
+    c->opt = opt;
+    if (lp->num_cons < 0 || lp->num_vars < 0 || lp->nnz < 0)
+      throw std::invalid_argument("matrix dimensions must be nonnegative");
+    CK(cudaSetDevice(opt.device));
+    cudaDeviceProp p{};
+    CK(cudaGetDeviceProperties(&p, opt.device));
+    if (p.major < 10)
+      throw CudaError("rhpdhg device library is built for sm_100a (B200); device is sm_" +
+                      std::to_string(p.major) + std::to_string(p.minor));
+    c->sm_count = p.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreate(&c->tev0));
+    CK(cudaEventCreate(&c->tev1));
+    build_layout(*lp, 0, lp->num_cons, c->L);
+    const HostLayout& L = c->L;
+    c->m = L.m;
+    c->n = L.n;
+    cudaStream_t s = c->stream;
+    upload_op(c->A, L.A, s);
+    upload_op(c->At, L.At, s);
+    const size_t m = static_cast<size_t>(c->m), n = static_cast<size_t>(c->n);
+    for (double** p2 : {&c->c, &c->vl, &c->vu, &c->co, &c->vlo, &c->vuo, &c->cs, &c->x, &c->aty,
+                        &c->x0, &c->aty0, &c->xp, &c->xout, &c->rcout, &c->pv, &c->pw})
+      *p2 = dev_alloc<double>(n);
+    for (double** p2 : {&c->cl, &c->cu, &c->clo, &c->cuo, &c->rs, &c->y, &c->ax, &c->y0, &c->ax0,
+                        &c->yp, &c->yout, &c->pav})
+      *p2 = dev_alloc<double>(m);
+    const std::vector<int32_t> lrows = local_rows(*c);
+    upload_perm(c->co, lp->objective, L.pcol, c->hbuf, s);
+    upload_perm(c->vlo, lp->var_lb, L.pcol, c->hbuf, s);
+    upload_perm(c->vuo, lp->var_ub, L.pcol, c->hbuf, s);
+    upload_perm(c->clo, lp->con_lb, L.prow, c->hbuf, s);
+    upload_perm(c->cuo, lp->con_ub, L.prow, c->hbuf, s);
+    CK(cudaMemcpyAsync(c->c, c->co, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->vl, c->vlo, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->vu, c->vuo, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->cl, c->clo, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->cu, c->cuo, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    c->hbuf.assign(std::max(m, n), 1.0);
+    upload(c->rs, c->hbuf.data(), m, s);
+    upload(c->cs, c->hbuf.data(), n, s);
+    CK(cudaStreamSynchronize(s));
+    // grids: persistent, a multiple of the SM count, never more than tiles
+    const int occ_a = std::max(occupancy_blocks((const void*)spmv_fused<EpiDual>),
+                               occupancy_blocks((const void*)spmv_fused<EpiKktRow>));
+    const int occ_at = std::max(occupancy_blocks((const void*)spmv_fused<EpiAty>),
+                                occupancy_blocks((const void*)spmv_fused<EpiKktCol>));
+    auto clampg = [](int64_t tiles, int64_t cap) {
+      return static_cast<int>(std::max<int64_t>(1, std::min(tiles, cap)));
+    };
+    c->grid_a = clampg(c->A.sched.total_tiles, (int64_t)c->sm_count * occ_a);
+    c->grid_at = clampg(c->At.sched.total_tiles, (int64_t)c->sm_count * occ_at);
+    c->grid_vec = vec_grid(*c, std::max<int64_t>(c->m, c->n));
+    c->grid_max = std::max({c->grid_a, c->grid_at, c->grid_vec});
+    for (double** p2 : {&c->part1, &c->part3, &c->partA, &c->partAt})
+      *p2 = dev_alloc<double>(static_cast<size_t>(c->grid_max) * 16);
+    c->hist = dev_alloc<double>(static_cast<size_t>(opt.block_limit));
+    CK(cudaMalloc(&c->ctl, sizeof(Ctl)));
+    CK(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));
+    std::memset(c->ctl_host, 0, sizeof(Ctl));
+    Ctl& h = *c->ctl_host;
+    h.graph_mode = opt.use_graph ? 1 : 0;
+    h.hist = c->hist;
+    h.block_limit = opt.block_limit;
+    h.check_interval = 64;
+    h.iteration_limit = INT64_MAX;
+    h.r_anchor = h.r_prev = std::numeric_limits<double>::infinity();
+    h.k1_token = -1;
+    CK(cudaMemcpy(c->ctl, c->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice));
+    for (double* p2 : {c->x, c->aty, c->x0, c->aty0, c->xp, c->xout, c->rcout, c->pv, c->pw})
+      CK(cudaMemsetAsync(p2, 0, std::max<size_t>(n, 1) * sizeof(double), s));
+    for (double* p2 : {c->y, c->ax, c->y0, c->ax0, c->yp, c->yout, c->pav})
+      CK(cudaMemsetAsync(p2, 0, std::max<size_t>(m, 1) * sizeof(double), s));
+    CK(cudaStreamSynchronize(s));
+  });
+  if (rc != RHPDHG_OK) {
+    rhp_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return RHPDHG_OK;
+}
+
+int rhp_destroy(rhp_ctx* c) {
+  if (!c) return RHPDHG_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  free_op(c->A);
+  free_op(c->At);
+  for (double* p : {c->c, c->vl, c->vu, c->cl, c->cu, c->co, c->vlo, c->vuo, c->clo, c->cuo,
+                    c->rs, c->cs, c->x, c->y, c->ax, c->aty, c->x0, c->y0, c->ax0, c->aty0,
+                    c->xp, c->yp, c->xout, c->yout, c->rcout, c->pv, c->pw, c->pav, c->part1,
+                    c->part3, c->partA, c->partAt, c->hist})
+    if (p) cudaFree(p);
+  if (c->ctl) cudaFree(c->ctl);
+  if (c->ctl_host) cudaFreeHost(c->ctl_host);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->tev0) cudaEventDestroy(c->tev0);
+  if (c->tev1) cudaEventDestroy(c->tev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return RHPDHG_OK;
+}
+
+int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
+  return guarded([&] {
+    std::memset(info, 0, sizeof(*info));
+    info->m_local = c->m;
+    info->n = c->n;
+    info->nnz_local = c->L.nnz;
+    for (int k = 0; k < 8; ++k) {
+      info->row_bins[k] = c->L.A.bin_rows[k];
+      info->col_bins[k] = c->L.At.bin_rows[k];
+    }
+    info->grid_a = c->grid_a;
+    info->grid_at = c->grid_at;
+    info->grid_vec = c->grid_vec;
+    info->sm_count = c->sm_count;
+  });
+}
+
+// ruiz_equilibrate + pock_chambolle_scale (scaling.cpp:46-81) on the device.
+int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    const int64_t m = c->m, n = c->n;
+    const int gr = vec_grid(*c, std::max<int64_t>(m, n));
+    if (enabled) {
+      // Ruiz on working copies of the original values (A.v and At.v hold
+      // the originals until the final apply)
+      double* rmax = c->pav;  // m scratch
+      double* cmax = c->pw;   // n scratch
+      double* wA = c->A.v;
+      double* wT = c->At.v;
+      for (int pass = 0; pass < ruiz_iterations; ++pass) {
+        k_row_absmax_sqrt<<<gr, kBlock, 0, s>>>(c->A.rp, wA, m, rmax);
+        k_row_absmax_sqrt<<<gr, kBlock, 0, s>>>(c->At.rp, wT, n, cmax);
+        k_ruiz_divide<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.ci, wA, m, rmax, cmax);
+        k_ruiz_divide<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, wT, n, cmax, rmax);
+        k_vec_div<<<gr, kBlock, 0, s>>>(c->rs, rmax, m);
+        k_vec_div<<<gr, kBlock, 0, s>>>(c->cs, cmax, n);
+      }
+      // apply_scales(original, rs, cs): values and vectors from the originals
+      k_scale_values<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.ci, c->A.v_orig, c->A.v, m, c->rs, c->cs);
+      k_scale_values<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v_orig, c->At.v, n, c->cs,
+                                           c->rs);
+      k_apply_col_scales<<<gr, kBlock, 0, s>>>(c->c, c->vl, c->vu, c->cs, n);
+      k_apply_row_scales<<<gr, kBlock, 0, s>>>(c->cl, c->cu, c->rs, m);
+      if (pock_chambolle) {
+        double* rn = c->pav;
+        double* cn = c->pw;
+        k_pc_rows<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.v, m, rn);
+        k_pc_cols<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v_orig, n, c->rs, c->cs, cn);
+        // apply_scales(ruiz-scaled, rn, cn) in place
+        k_scale_values<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.ci, c->A.v, c->A.v, m, rn, cn);
+        k_scale_values<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v, c->At.v, n, cn, rn);
+        k_apply_col_scales<<<gr, kBlock, 0, s>>>(c->c, c->vl, c->vu, cn, n);
+        k_apply_row_scales<<<gr, kBlock, 0, s>>>(c->cl, c->cu, rn, m);
+        k_vec_mul<<<gr, kBlock, 0, s>>>(c->rs, rn, m);
+        k_vec_mul<<<gr, kBlock, 0, s>>>(c->cs, cn, n);
+      }
+      CK(cudaGetLastError());
+    }
+    // the original values are no longer needed on the device
+    CK(cudaStreamSynchronize(s));
+    if (c->A.v_orig) CK(cudaFree(c->A.v_orig));
+    if (c->At.v_orig) CK(cudaFree(c->At.v_orig));
+    c->A.v_orig = c->At.v_orig = nullptr;
+  });
+}
+
+int rhp_get_scaled(rhp_ctx* c, const rhp_scaled_out* o) {
+  return guarded([&] {
+    const HostLayout& L = c->L;
+    const std::vector<int32_t> lrows = local_rows(*c);
+    auto pull = [&](double* dst, const double* src, size_t cnt) {
+      std::vector<double> t(cnt);
+      if (cnt) CK(cudaMemcpy(t.data(), src, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+      return t;
+    };
+    if (o->csr_values) {
+      auto t = pull(nullptr, c->A.v, static_cast<size_t>(L.nnz));
+      for (size_t e = 0; e < t.size(); ++e) o->csr_values[L.a_dev_to_csr[e]] = t[e];
+    }
+    if (o->csc_values) {
+      auto t = pull(nullptr, c->At.v, static_cast<size_t>(L.nnz));
+      for (size_t e = 0; e < t.size(); ++e) o->csc_values[L.at_dev_to_csc[e]] = t[e];
+    }
+    if (o->row_scale) download_perm(o->row_scale, c->rs, lrows, c->hbuf, c->stream);
+    if (o->col_scale) download_perm(o->col_scale, c->cs, L.pcol, c->hbuf, c->stream);
+    if (o->objective) download_perm(o->objective, c->c, L.pcol, c->hbuf, c->stream);
+    if (o->var_lb) download_perm(o->var_lb, c->vl, L.pcol, c->hbuf, c->stream);
+    if (o->var_ub) download_perm(o->var_ub, c->vu, L.pcol, c->hbuf, c->stream);
+    if (o->con_lb) download_perm(o->con_lb, c->cl, lrows, c->hbuf, c->stream);
+    if (o->con_ub) download_perm(o->con_ub, c->cu, lrows, c->hbuf, c->stream);
+  });
+}
+
+int rhp_power_begin(rhp_ctx* c, const double* v0) {
+  return guarded([&] { upload_perm(c->pv, v0, c->L.pcol, c->hbuf, c->stream); });
+}
+
+int rhp_power_step(rhp_ctx* c, double* vw, double* ww) {
+  return guarded([&] {
+    launch_spmv(*c, c->A, c->grid_a, c->pv, EpiStore{c->pav}, nullptr, nullptr, c->stream);
+    EpiPowerW e{c->ctl, c->pv, c->pw};
+    launch_spmv(*c, c->At, c->grid_at, c->pav, e, c->partAt, &c->ctl->ticket_pow, c->stream);
+    pull_ctl(*c);
+    *vw = c->ctl_host->pw_vw;
+    *ww = c->ctl_host->pw_ww;
+  });
+}
+
+int rhp_power_normalize(rhp_ctx* c, double wnorm) {
+  return guarded([&] {
+    k_normalize<<<c->grid_vec, kBlock, 0, c->stream>>>(c->pv, c->pw, wnorm, c->n);
+    CK(cudaGetLastError());
+  });
+}
+
+int rhp_spmv(rhp_ctx* c, int transpose, const double* in, double* out) {
+  return guarded([&] {
+    const std::vector<int32_t> lrows = local_rows(*c);
+    if (!transpose) {
+      upload_perm(c->pv, in, c->L.pcol, c->hbuf, c->stream);
+      launch_spmv(*c, c->A, c->grid_a, c->pv, EpiStore{c->pav}, nullptr, nullptr, c->stream);
+      download_perm(out, c->pav, lrows, c->hbuf, c->stream);
+    } else {
+      upload_perm(c->pav, in, lrows, c->hbuf, c->stream);
+      launch_spmv(*c, c->At, c->grid_at, c->pav, EpiStore{c->pw}, nullptr, nullptr, c->stream);
+      download_perm(out, c->pw, c->L.pcol, c->hbuf, c->stream);
+    }
+  });
+}
+
+int rhp_set_step(rhp_ctx* c, const rhp_step* st) {
+  return guarded([&] {
+    pull_ctl(*c);
+    Ctl& h = *c->ctl_host;
+    h.eta = st->eta;
+    h.omega = st->omega;
+    h.gamma = st->gamma;
+    h.tau = st->tau;
+    h.sigma = st->sigma;
+    h.sigma_inv = st->sigma_inv;
+    h.primal_scale = st->primal_scale;
+    h.dual_scale = st->dual_scale;
+    h.beta_s = st->beta_sufficient;
+    h.beta_n = st->beta_necessary;
+    h.beta_a = st->beta_artificial;
+    h.check_interval = st->check_interval;
+    h.iteration_limit = st->iteration_limit;
+    h.restarts_enabled = st->restarts_enabled;
+    h.record_history = st->record_history;
+    c->host_check_interval = st->check_interval;
+    c->host_iteration_limit = st->iteration_limit;
+    CK(cudaMemcpyAsync(c->ctl, c->ctl_host, offsetof(Ctl, k), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rhp_reset_iterate(rhp_ctx* c) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    const size_t m = static_cast<size_t>(std::max<int64_t>(c->m, 1));
+    const size_t n = static_cast<size_t>(std::max<int64_t>(c->n, 1));
+    for (double* p : {c->x, c->aty, c->x0, c->aty0, c->xp})
+      CK(cudaMemsetAsync(p, 0, n * sizeof(double), s));
+    for (double* p : {c->y, c->ax, c->y0, c->ax0, c->yp})
+      CK(cudaMemsetAsync(p, 0, m * sizeof(double), s));
+    pull_ctl(*c);
+    Ctl& h = *c->ctl_host;
+    h.k = 0;
+    h.total = 0;
+    h.block_iters = 0;
+    h.r_anchor = h.r_prev = std::numeric_limits<double>::infinity();
+    h.r_last = 0.0;
+    h.stop = h.verdict = h.check_due = h.breakdown = 0;
+    h.k1_token = -1;
+    h.x_dist2 = h.y_dist2 = h.x_norm2 = h.y_norm2 = 0.0;
+    CK(cudaMemcpyAsync(c->ctl, c->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    c->host_total = 0;
+  });
+}
+
+int rhp_set_iterate(rhp_ctx* c, const double* x, const double* y) {
+  return guarded([&] {
+    upload_perm(c->x, x, c->L.pcol, c->hbuf, c->stream);
+    upload_perm(c->y, y, local_rows(*c), c->hbuf, c->stream);
+    exact_caches(*c);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rhp_run_block(rhp_ctx* c, rhp_block_out* out) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    CK(cudaEventRecord(c->ev0, s));
+    if (c->opt.use_graph) {
+      if (!c->graph_built) build_graph(*c);
+      CK(cudaGraphLaunch(c->gexec, s));
+    } else {
+      // plain launches: enough iterations to reach the next stop point;
+      // kernels of iterations past the stop exit at entry
+      int64_t L = c->opt.block_limit;
+      const int64_t ci = c->host_check_interval;
+      L = std::min<int64_t>(L, ci - (c->host_total % ci));
+      if (c->host_iteration_limit != INT64_MAX)
+        L = std::min<int64_t>(L, std::max<int64_t>(1, c->host_iteration_limit - c->host_total));
+      launch_primal_init(*c, s);
+      for (int64_t i = 0; i < L; ++i) launch_iteration(*c, static_cast<int>(i), s);
+    }
+    CK(cudaEventRecord(c->ev1, s));
+    pull_ctl(*c);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->last_block_ms = ms;
+    const Ctl& h = *c->ctl_host;
+    c->host_total = h.total;
+    out->iterations_done = h.block_iters;
+    out->total = h.total;
+    out->k = h.k;
+    out->verdict = h.verdict;
+    out->check_due = h.check_due;
+    out->breakdown = h.breakdown;
+    out->r_last = h.r_last;
+    out->r_anchor = h.r_anchor;
+    out->r_prev = h.r_prev;
+    out->q_last = h.q_last;
+    out->x_dist2 = h.x_dist2;
+    out->y_dist2 = h.y_dist2;
+    out->x_norm2 = h.x_norm2;
+    out->y_norm2 = h.y_norm2;
+  });
+}
+
+int rhp_get_history(rhp_ctx* c, double* out, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    const int64_t k = std::min<int64_t>(c->ctl_host->block_iters, cap);
+    if (k > 0) CK(cudaMemcpy(out, c->hist, static_cast<size_t>(k) * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+    *count = k;
+  });
+}
+
+int rhp_kkt(rhp_ctx* c, int which, rhp_kkt_sums* out) {
+  return guarded([&] {
+    if (which == 0) run_kkt(*c, c->x, c->y, true, true, out);
+    else run_kkt(*c, c->xp, c->yp, false, false, out);
+  });
+}
+
+int rhp_kkt_of(rhp_ctx* c, const double* x, const double* y, rhp_kkt_sums* out) {
+  return guarded([&] {
+    // scratch: pv (n) and pav (m); the scales are still 1 before rhp_scale
+    upload_perm(c->pv, x, c->L.pcol, c->hbuf, c->stream);
+    upload_perm(c->pav, y, local_rows(*c), c->hbuf, c->stream);
+    run_kkt(*c, c->pv, c->pav, false, false, out);
+  });
+}
+
+int rhp_fetch_solution(rhp_ctx* c, double* x, double* y, double* rcost) {
+  return guarded([&] {
+    if (x) download_perm(x, c->xout, c->L.pcol, c->hbuf, c->stream);
+    if (y) download_perm(y, c->yout, local_rows(*c), c->hbuf, c->stream);
+    if (rcost) download_perm(rcost, c->rcout, c->L.pcol, c->hbuf, c->stream);
+  });
+}
+
+int rhp_fetch_iterate(rhp_ctx* c, double* x, double* y, double* ax, double* aty) {
+  return guarded([&] {
+    const std::vector<int32_t> lrows = local_rows(*c);
+    if (x) download_perm(x, c->x, c->L.pcol, c->hbuf, c->stream);
+    if (y) download_perm(y, c->y, lrows, c->hbuf, c->stream);
+    if (ax) download_perm(ax, c->ax, lrows, c->hbuf, c->stream);
+    if (aty) download_perm(aty, c->aty, c->L.pcol, c->hbuf, c->stream);
+  });
+}
+
+int rhp_restart(rhp_ctx* c) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    const size_t m = static_cast<size_t>(c->m), n = static_cast<size_t>(c->n);
+    if (n) {
+      CK(cudaMemcpyAsync(c->x0, c->x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(c->aty0, c->aty, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    if (m) {
+      CK(cudaMemcpyAsync(c->y0, c->y, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(c->ax0, c->ax, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    const double inf = std::numeric_limits<double>::infinity();
+    const int64_t zero = 0;
+    SET_CTL(*c, k, zero);
+    SET_CTL(*c, r_anchor, inf);
+    SET_CTL(*c, r_prev, inf);
+  });
+}
+
+int rhp_last_block_ms(rhp_ctx* c, double* ms) {
+  *ms = c->last_block_ms;
+  return RHPDHG_OK;
+}
+
+int rhp_timer(rhp_ctx* c, int start, double* ms) {
+  return guarded([&] {
+    if (start) {
+      CK(cudaEventRecord(c->tev0, c->stream));
+      if (ms) *ms = 0.0;
+    } else {
+      CK(cudaEventRecord(c->tev1, c->stream));
+      CK(cudaEventSynchronize(c->tev1));
+      float f = 0.f;
+      CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+      if (ms) *ms = f;
+    }
+  });
+}
+
+// Times `reps` back-to-back launches of each fused iteration kernel on the
+// live iterate (CUDA events on the ctx stream). Mutates the iterate: call
+// after the measured solve work is done.
+int rhp_time_kernels(rhp_ctx* c, int reps, double* ms_k1, double* ms_k2, double* ms_k3) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    pull_ctl(*c);
+    const int32_t gm = c->ctl_host->graph_mode;
+    const int32_t zero = 0, one = 1;
+    SET_CTL(*c, graph_mode, zero);
+    SET_CTL(*c, bench, one);
+    float f = 0.f;
+    CK(cudaEventRecord(c->tev0, s));
+    for (int r = 0; r < reps; ++r) launch_primal_init(*c, s);
+    CK(cudaEventRecord(c->tev1, s));
+    CK(cudaEventSynchronize(c->tev1));
+    CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+    if (ms_k3) *ms_k3 = f / reps;
+    CK(cudaEventRecord(c->tev0, s));
+    for (int r = 0; r < reps; ++r)
+      launch_spmv(*c, c->A, c->grid_a, c->xp, epi_dual(*c, 0), c->part1, &c->ctl->ticket_dual, s);
+    CK(cudaEventRecord(c->tev1, s));
+    CK(cudaEventSynchronize(c->tev1));
+    CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+    if (ms_k1) *ms_k1 = f / reps;
+    CK(cudaEventRecord(c->tev0, s));
+    for (int r = 0; r < reps; ++r)
+      launch_spmv(*c, c->At, c->grid_at, c->yp, epi_aty(*c, 0), c->part3, nullptr, s);
+    CK(cudaEventRecord(c->tev1, s));
+    CK(cudaEventSynchronize(c->tev1));
+    CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+    if (ms_k2) *ms_k2 = f / reps;
+    SET_CTL(*c, bench, zero);
+    SET_CTL(*c, graph_mode, gm);
+  });
+}
+
+int rhp_synchronize(rhp_ctx* c) {
+  return guarded([&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+}  // extern "C"

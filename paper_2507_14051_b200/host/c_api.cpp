@@ -1,0 +1,282 @@
+// c_api.cpp — the flat C ABI of include/rhpdhg_c.h over the C++ API.
+#include <cstring>
+#include <memory>
+#include <exception>
+#include <string>
+
+#include "device.hpp"
+#include "rhpdhg/errors.hpp"
+#include "rhpdhg/solver.hpp"
+#include "rhpdhg/termination.hpp"
+#include "rhpdhg_c.h"
+#include "session.hpp"
+
+using namespace rhpdhg;
+
+namespace {
+thread_local std::string g_msg;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RHPDHG_OK;
+  } catch (const UsageError& e) {
+    g_msg = e.what();
+    return RHPDHG_E_USAGE;
+  } catch (const InvalidProblemError& e) {
+    g_msg = e.what();
+    return RHPDHG_E_INVALID_PROBLEM;
+  } catch (const ParseError& e) {
+    g_msg = e.what();
+    return RHPDHG_E_PARSE;
+  } catch (const NumericalBreakdownError& e) {
+    g_msg = e.what();
+    return RHPDHG_E_BREAKDOWN;
+  } catch (const DeviceError& e) {
+    g_msg = e.what();
+    return RHPDHG_E_DEVICE;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return RHPDHG_E_INTERNAL;
+  }
+}
+
+LpProblem to_problem(const rhpdhg_lp_view* v) {
+  if (!v) throw UsageError("null LP view");
+  if (v->num_cons < 0 || v->num_vars < 0) throw UsageError("matrix dimensions must be nonnegative");
+  const size_t m = static_cast<size_t>(v->num_cons), n = static_cast<size_t>(v->num_vars);
+  const Index nz = (v->num_cons > 0 && v->row_ptr) ? v->row_ptr[v->num_cons] : 0;
+  std::vector<Index> rp = v->row_ptr ? std::vector<Index>(v->row_ptr, v->row_ptr + m + 1)
+                                     : std::vector<Index>(m + 1, 0);
+  LpProblem p;
+  p.matrix = SparseMatrix::from_csr(v->num_cons, v->num_vars, std::move(rp),
+                                    std::vector<Index>(v->col_index, v->col_index + nz),
+                                    std::vector<double>(v->values, v->values + nz));
+  p.objective.assign(v->objective, v->objective + n);
+  p.objective_offset = v->objective_offset;
+  p.var_lb.assign(v->var_lb, v->var_lb + n);
+  p.var_ub.assign(v->var_ub, v->var_ub + n);
+  p.con_lb.assign(v->con_lb, v->con_lb + m);
+  p.con_ub.assign(v->con_ub, v->con_ub + m);
+  p.maximization = v->maximization != 0;
+  return p;
+}
+
+SolverConfig to_config(const rhpdhg_config_c* c) {
+  SolverConfig s;
+  if (!c) return s;
+  s.scaling_enabled = c->scaling_enabled != 0;
+  s.ruiz_iterations = c->ruiz_iterations;
+  s.pock_chambolle = c->pock_chambolle != 0;
+  s.restarts_enabled = c->restarts_enabled != 0;
+  s.stepsize_multiplier = c->stepsize_multiplier;
+  s.power_tol = c->power_tol;
+  s.power_max_iters = c->power_max_iters;
+  s.power_seed = c->power_seed;
+  s.beta_sufficient = c->beta_sufficient;
+  s.beta_necessary = c->beta_necessary;
+  s.beta_artificial = c->beta_artificial;
+  s.reflection_gamma = c->reflection_gamma;
+  s.pid_kp = c->pid_kp;
+  s.pid_ki = c->pid_ki;
+  s.pid_kd = c->pid_kd;
+  s.initial_weight = c->initial_weight;
+  s.epsilon = c->epsilon;
+  s.check_interval = c->check_interval;
+  s.time_limit_seconds = c->time_limit_seconds;
+  s.iteration_limit = c->iteration_limit;
+  s.verbosity = c->verbosity;
+  s.record_residual_history = c->record_residual_history != 0;
+  return s;
+}
+
+void to_c(const KktResiduals& r, rhpdhg_kkt_c* o) {
+  *o = rhpdhg_kkt_c{r.gap_abs,    r.gap_rel,   r.primal_inf, r.primal_rel,  r.dual_eq,
+                    r.dual_cone,  r.gap_denom, r.primal_denom, r.dual_denom};
+}
+
+void fill_report(const SolutionReport& r, rhpdhg_report_c* out, double* x, double* y, double* rc,
+                 double* hist, int64_t hist_cap);
+}  // namespace
+
+struct rhpdhg_session {
+  LpProblem problem;
+  std::unique_ptr<Session> session;
+};
+
+extern "C" {
+
+const char* rhpdhg_last_error(void) { return g_msg.c_str(); }
+
+int rhpdhg_config_default(rhpdhg_config_c* c) {
+  return guarded([&] {
+    const SolverConfig s;
+    std::memset(c, 0, sizeof(*c));
+    c->scaling_enabled = s.scaling_enabled;
+    c->ruiz_iterations = s.ruiz_iterations;
+    c->pock_chambolle = s.pock_chambolle;
+    c->restarts_enabled = s.restarts_enabled;
+    c->stepsize_multiplier = s.stepsize_multiplier;
+    c->power_tol = s.power_tol;
+    c->power_max_iters = s.power_max_iters;
+    c->power_seed = s.power_seed;
+    c->beta_sufficient = s.beta_sufficient;
+    c->beta_necessary = s.beta_necessary;
+    c->beta_artificial = s.beta_artificial;
+    c->reflection_gamma = s.reflection_gamma;
+    c->pid_kp = s.pid_kp;
+    c->pid_ki = s.pid_ki;
+    c->pid_kd = s.pid_kd;
+    c->initial_weight = s.initial_weight;
+    c->epsilon = s.epsilon;
+    c->check_interval = s.check_interval;
+    c->time_limit_seconds = s.time_limit_seconds;
+    c->iteration_limit = s.iteration_limit;
+    c->verbosity = s.verbosity;
+    c->record_residual_history = s.record_residual_history;
+  });
+}
+
+int rhpdhg_set_device(int device) {
+  return guarded([&] { default_device_options().device = device; });
+}
+
+int rhpdhg_set_device_options(int device, int use_graph, int64_t block_limit) {
+  return guarded([&] {
+    if (block_limit < 1) throw UsageError("block_limit must be >= 1");
+    DeviceOptions& d = default_device_options();
+    d.device = device;
+    d.use_graph = use_graph != 0;
+    d.block_limit = static_cast<long>(block_limit);
+  });
+}
+
+int rhpdhg_solve_csr(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg, rhpdhg_report_c* out,
+                     double* x, double* y, double* rc, double* hist, int64_t hist_cap) {
+  return guarded([&] {
+    const LpProblem p = to_problem(lp);
+    fill_report(solve(p, to_config(cfg)), out, x, y, rc, hist, hist_cap);
+  });
+}
+
+int rhpdhg_session_create(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg,
+                          rhpdhg_session** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<rhpdhg_session>();
+    h->problem = to_problem(lp);
+    h->session = std::make_unique<Session>(h->problem, to_config(cfg), default_device_options());
+    *out = h.release();
+  });
+}
+
+int rhpdhg_session_advance(rhpdhg_session* s, int64_t iterations, int32_t* running) {
+  return guarded([&] {
+    const bool r = s->session->advance(static_cast<long>(iterations));
+    if (running) *running = r ? 1 : 0;
+  });
+}
+
+int rhpdhg_session_info(rhpdhg_session* s, int64_t* total, int64_t* restarts, rhpdhg_kkt_c* last,
+                        double* setup_seconds, int64_t* blocks, int64_t* checks) {
+  return guarded([&] {
+    if (total) *total = s->session->total();
+    if (restarts) *restarts = s->session->restarts();
+    if (last) to_c(s->session->last_residuals(), last);
+    if (setup_seconds) *setup_seconds = s->session->setup_seconds();
+    if (blocks) *blocks = s->session->device_blocks();
+    if (checks) *checks = s->session->kkt_checks();
+  });
+}
+
+int rhpdhg_session_timer(rhpdhg_session* s, int start, double* ms) {
+  return guarded([&] { detail::ok(rhp_timer(s->session->device(), start, ms), "rhp_timer"); });
+}
+
+int rhpdhg_session_time_kernels(rhpdhg_session* s, int reps, double* ms3) {
+  return guarded([&] {
+    detail::ok(rhp_time_kernels(s->session->device(), reps, &ms3[0], &ms3[1], &ms3[2]),
+               "rhp_time_kernels");
+  });
+}
+
+int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
+  return guarded([&] {
+    rhp_layout_info li{};
+    detail::ok(rhp_layout(s->session->device(), &li), "rhp_layout");
+    o[0] = li.m_local;
+    o[1] = li.n;
+    o[2] = li.nnz_local;
+    for (int k = 0; k < 8; ++k) {
+      o[3 + k] = li.row_bins[k];
+      o[11 + k] = li.col_bins[k];
+    }
+    o[19] = li.grid_a;
+    o[20] = li.grid_at;
+    o[21] = li.grid_vec;
+    o[22] = li.sm_count;
+    o[23] = o[24] = o[25] = o[26] = 0;
+  });
+}
+
+int rhpdhg_session_finish(rhpdhg_session* s, rhpdhg_report_c* out, double* x, double* y,
+                          double* rc, double* hist, int64_t hist_cap) {
+  return guarded([&] { fill_report(s->session->finish(), out, x, y, rc, hist, hist_cap); });
+}
+
+void rhpdhg_session_destroy(rhpdhg_session* s) { delete s; }
+
+}  // extern "C"
+
+namespace {
+void fill_report(const SolutionReport& r, rhpdhg_report_c* out, double* x, double* y, double* rc,
+                 double* hist, int64_t hist_cap) {
+  {
+    std::memset(out, 0, sizeof(*out));
+    out->status = static_cast<int32_t>(r.status);
+    out->objective = r.objective;
+    to_c(r.residuals, &out->residuals);
+    out->iterations = r.iterations;
+    out->restart_count = r.restart_count;
+    out->wall_time_seconds = r.wall_time_seconds;
+    out->final_fixed_point_residual = r.final_fixed_point_residual;
+    out->final_primal_weight = r.final_primal_weight;
+    out->matrix_norm_estimate = r.matrix_norm_estimate;
+    out->power_iterations = r.power_iterations;
+    out->spmv_loop = r.spmv_loop;
+    out->spmv_checks = r.spmv_checks;
+    out->spmv_setup = r.spmv_setup;
+    out->kkt_checks = r.kkt_checks;
+    out->has_inner_residuals = r.inner_residuals ? 1 : 0;
+    if (r.inner_residuals) to_c(*r.inner_residuals, &out->inner_residuals);
+    out->history_len = static_cast<int64_t>(r.fixed_point_residual_history.size());
+    out->setup_seconds = r.setup_seconds;
+    out->loop_seconds = r.loop_seconds;
+    out->device_blocks = r.device_blocks;
+    if (x) std::memcpy(x, r.x.data(), r.x.size() * sizeof(double));
+    if (y) std::memcpy(y, r.y.data(), r.y.size() * sizeof(double));
+    if (rc) std::memcpy(rc, r.reduced_costs.data(), r.reduced_costs.size() * sizeof(double));
+    if (hist && hist_cap > 0) {
+      const size_t k = std::min<size_t>(r.fixed_point_residual_history.size(),
+                                        static_cast<size_t>(hist_cap));
+      std::memcpy(hist, r.fixed_point_residual_history.data(), k * sizeof(double));
+    }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int rhpdhg_kkt_residuals(const rhpdhg_lp_view* lp, const double* x, const double* y,
+                         rhpdhg_kkt_c* out) {
+  return guarded([&] {
+    const LpProblem p = to_problem(lp);
+    const KktResiduals r = kkt_residuals(
+        p, std::span<const double>(x, static_cast<size_t>(p.num_vars())),
+        std::span<const double>(y, static_cast<size_t>(p.num_cons())));
+    to_c(r, out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// session.hpp — internal: the solve() state machine (setup in the ctor,
+// one device block + host control per step(), report in finish()).
+#pragma once
+
+#include <chrono>
+#include <memory>
+
+#include "device.hpp"
+#include "kkt.hpp"
+#include "rhpdhg/config.hpp"
+#include "rhpdhg/pdhg.hpp"
+#include "rhpdhg/report.hpp"
+#include "rhpdhg/restart.hpp"
+#include "rhpdhg/solver.hpp"
+
+namespace rhpdhg {
+
+using Clock = std::chrono::steady_clock;
+
+class Session {
+ public:
+  Session(const LpProblem& problem, const SolverConfig& cfg, const DeviceOptions& dopt);
+  ~Session();
+  bool step();                   // false once decided
+  bool advance(long iterations); // runs blocks until >= iterations more are done or decided
+  SolutionReport finish();
+  long total() const { return total_; }
+  bool decided() const { return decided_; }
+  long restarts() const { return restarts_; }
+  long device_blocks() const { return report_.device_blocks; }
+  long kkt_checks() const { return report_.kkt_checks; }
+  const KktResiduals& last_residuals() const { return last_; }
+  double setup_seconds() const { return report_.setup_seconds; }
+  rhp_ctx* device() const;
+
+ private:
+  KktResiduals kkt_check(int which);
+
+  const LpProblem& problem_;
+  SolverConfig cfg_;
+  std::unique_ptr<detail::Device> dev_;
+  Clock::time_point t0_, t_loop_;
+  StepConfig step_;
+  PidState pid_;
+  detail::Denoms denoms_{1.0, 1.0};
+  ToleranceConfig tol_;
+  SolutionReport report_;
+  KktResiduals last_;
+  SolveStatus status_ = SolveStatus::iteration_limit;
+  bool decided_ = false, have_inner_ = false;
+  long total_ = 0, restarts_ = 0;
+  std::uint64_t spmv_checks_ = 0;
+  double last_fpr_ = std::numeric_limits<double>::infinity();
+};
+
+}  // namespace rhpdhg

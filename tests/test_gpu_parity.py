@@ -1,0 +1,255 @@
+"""GPU parity suite (-m gpu): the CUDA product, driven through its C ABIs,
+against the oracle (oracle/rhpdhg_oracle.c, bit-identical to the reference,
+see test_oracle.py) and against the golden fixtures generated from the
+reference (tests/golden/).
+
+Tolerances (BASELINE.json north star):
+  * SpMV: |gpu - ref| <= 1e-14 * (|A| |x|)_i  (sum-order/FMA drift only)
+  * scaling (Ruiz + Pock-Chambolle): bit-identical
+  * first 100 iterates: max |dz| <= 1e-10 * max(1, max |z_ref|)
+  * final objective: 1e-6 relative; KKT of the returned point at the solve's
+    epsilon (re-evaluated by the oracle); status equal.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import support
+from paper_2507_14051_b200 import LpProblem, SolverConfig, kkt_residuals, set_device_options, solve
+from paper_2507_14051_b200.device import DeviceContext
+from paper_2507_14051_b200.generators import c1_small, c3_transport, random_rows_lp
+
+pytestmark = pytest.mark.gpu
+
+RANDOM = support.load_golden("random_feasible.json")["instances"]
+ANALYTIC = support.load_golden("analytic_lps.json")["instances"]
+SUITE = support.load_golden("random_suite.json")["instances"]
+INF = math.inf
+
+
+def ragged_lp():
+    """Every bin of the schedule: empty rows, 1-nnz rows, each sub-warp width,
+    CTA rows (>512) and multi-chunk rows (>8192 nnz)."""
+    lengths = np.array([0, 1, 2, 3, 4, 5, 8, 9, 16, 17, 32, 33, 64, 65, 300, 512, 513, 700, 4000,
+                        8192, 8193, 20000] + [7] * 300 + [0] * 20 + [1] * 50)
+    rng = np.random.default_rng(11)
+    rng.shuffle(lengths)
+    return random_rows_lp(21, lengths.size, 25000, lengths, name="ragged")
+
+
+def cases():
+    out = [support.lp_from_json(i["lp"]) for i in RANDOM]
+    out += [ragged_lp(), c1_small(m=500, n=900), c3_transport(S=40, T=70),
+            LpProblem(3, 4, [0, 0, 0, 0], [], [], np.ones(4), np.zeros(4), np.ones(4),
+                      np.zeros(3), np.ones(3), name="empty"),
+            LpProblem(0, 3, [0], [], [], [2.0, -1.0, 0.5], [-1.0, -2.0, 0.25], [4.0, 3.0, 5.0],
+                      [], [], name="rowless")]
+    return out
+
+
+CASES = cases()
+
+
+def max_rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.size == 0:
+        return 0.0
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+@pytest.mark.parametrize("lp", CASES, ids=[c.name or str(i) for i, c in enumerate(CASES)])
+def test_spmv_matches_oracle(gpu, lp):
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, lp.num_vars)
+    y = rng.uniform(-1, 1, lp.num_cons)
+    absA = LpProblem(lp.num_cons, lp.num_vars, lp.row_ptr, lp.col_index, np.abs(lp.values),
+                     lp.objective, lp.var_lb, lp.var_ub, lp.con_lb, lp.con_ub)
+    O = support.oracle()
+    with DeviceContext(lp) as dev:
+        ax, aty = dev.spmv(x), dev.spmv(y, True)
+    bound_ax = support.spmv_with(O, absA, np.abs(x)) * 1e-14 + 1e-300
+    bound_aty = support.spmv_with(O, absA, np.abs(y), True) * 1e-14 + 1e-300
+    assert np.all(np.abs(ax - support.spmv_with(O, lp, x)) <= bound_ax)
+    assert np.all(np.abs(aty - support.spmv_with(O, lp, y, True)) <= bound_aty)
+
+
+@pytest.mark.parametrize("inst", RANDOM, ids=[i["name"] for i in RANDOM])
+def test_spmv_matches_reference_golden(gpu, inst):
+    lp = support.lp_from_json(inst["lp"])
+    sp = inst["spmv"]
+    with DeviceContext(lp) as dev:
+        assert max_rel(dev.spmv(sp["x"]), sp["ax"]) <= 1e-14
+        assert max_rel(dev.spmv(sp["y"], True), sp["aty"]) <= 1e-14
+
+
+@pytest.mark.parametrize("lp", CASES[:-2], ids=[c.name or str(i) for i, c in enumerate(CASES[:-2])])
+def test_scaling_bitwise_equal_to_oracle(gpu, lp):
+    for ruiz, pc in ((10, True), (10, False), (0, True), (3, True)):
+        want = support.scale_with(support.oracle(), lp, ruiz, pc)
+        with DeviceContext(lp) as dev:
+            dev.scale(True, ruiz, pc)
+            got = dev.get_scaled()
+        for k in want:
+            assert np.array_equal(got[k], want[k]), (k, ruiz, pc)
+
+
+@pytest.mark.parametrize("inst", RANDOM, ids=[i["name"] for i in RANDOM])
+def test_scaling_matches_reference_golden(gpu, inst):
+    lp = support.lp_from_json(inst["lp"])
+    with DeviceContext(lp) as dev:
+        dev.scale()
+        got = dev.get_scaled()
+    for k, v in inst["scaling"].items():
+        assert got[k].tolist() == v, k
+
+
+@pytest.mark.parametrize("inst", RANDOM, ids=[i["name"] for i in RANDOM])
+def test_first_100_iterates_match_reference(gpu, inst):
+    """Iterates after k = 1..100 iterations (full pipeline incl. scaling,
+    power iteration, restarts, KKT cache refreshes at 64) agree with the
+    reference within 1e-10 relative."""
+    lp = support.lp_from_json(inst["lp"])
+    for k, snap in inst["snapshots"].items():
+        r = solve(lp, SolverConfig(epsilon=1e-300, iteration_limit=int(k)))
+        assert r.iterations == int(k)
+        assert max_rel(r.x, snap["x"]) <= 1e-10, k
+        assert max_rel(r.y, snap["y"]) <= 1e-10, k
+
+
+@pytest.mark.parametrize("inst", ANALYTIC, ids=[i["name"] for i in ANALYTIC])
+@pytest.mark.parametrize("eps", ["0.0001", "1e-08"])
+def test_analytic_fixtures_match_reference(gpu, inst, eps):
+    lp = support.lp_from_json(inst["lp"])
+    want = inst["results"][eps]
+    r = solve(lp, SolverConfig(epsilon=float(eps)))
+    assert r.status == want["status"] == "optimal"
+    assert abs(r.objective - want["objective"]) <= 1e-6 * max(1.0, abs(want["objective"]))
+    assert r.matrix_norm_estimate == pytest.approx(want["matrix_norm_estimate"], rel=1e-12)
+    assert r.power_iterations == want["power_iterations"]
+    # tiny analytic LPs have <= 3 terms per row: the trajectory is reproduced
+    assert (r.iterations, r.restart_count, r.kkt_checks) == \
+        (want["iterations"], want["restart_count"], want["kkt_checks"])
+
+
+@pytest.mark.parametrize("inst", SUITE, ids=[i["name"] for i in SUITE])
+def test_random_suite_objective_and_kkt(gpu, inst):
+    lp = support.lp_from_json(inst["lp"])
+    want = inst["result_1e-8_cap20k"]
+    r = solve(lp, SolverConfig(epsilon=1e-8, iteration_limit=20000))
+    assert r.status == want["status"] == "optimal"
+    assert abs(r.objective - want["objective"]) <= 1e-6 * max(1.0, abs(want["objective"]))
+    h = inst["highs_objective"]
+    assert abs(r.objective - h) <= 1e-5 * max(1.0, abs(h))
+    k = support.kkt_with(support.oracle(), lp, r.x, r.y)
+    assert k["gap_rel"] <= 1e-8 and k["primal_rel"] <= 1e-8
+    assert k["dual_eq"] <= 1e-8 * k["dual_denom"]
+
+
+def test_solver_parity_c1(gpu):
+    lp = c1_small()
+    for eps in (1e-4, 1e-8):
+        cfg = SolverConfig(epsilon=eps)
+        g = solve(lp, cfg)
+        o = support.solve_with(support.oracle(), lp, cfg)
+        assert g.status == o.status == "optimal"
+        assert abs(g.objective - o.objective) <= 1e-6 * max(1.0, abs(o.objective))
+        k = support.kkt_with(support.oracle(), lp, g.x, g.y)
+        assert k["gap_rel"] <= eps and k["primal_rel"] <= eps
+        assert k["dual_eq"] <= eps * k["dual_denom"]
+        assert g.matrix_norm_estimate == pytest.approx(o.matrix_norm_estimate, rel=1e-12)
+
+
+def test_solves_are_bitwise_deterministic(gpu):
+    lp = c1_small(m=300, n=500)
+    a = solve(lp, SolverConfig(epsilon=1e-8))
+    b = solve(lp, SolverConfig(epsilon=1e-8))
+    assert a.iterations == b.iterations and a.restart_count == b.restart_count
+    assert a.objective == b.objective
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.y, b.y)
+
+
+def test_graph_and_plain_launch_modes_agree_bitwise(gpu):
+    lp = support.lp_from_json(RANDOM[-1]["lp"])
+    cfg = SolverConfig(epsilon=1e-8, record_residual_history=True)
+    try:
+        set_device_options(0, True, 64)
+        a = solve(lp, cfg)
+        set_device_options(0, False, 64)
+        b = solve(lp, cfg)
+        set_device_options(0, True, 7)
+        c = solve(lp, cfg)
+    finally:
+        set_device_options(0, True, 64)
+    for r in (b, c):
+        assert r.iterations == a.iterations and r.objective == a.objective
+        assert np.array_equal(r.x, a.x) and np.array_equal(r.y, a.y)
+        assert np.array_equal(r.fixed_point_residual_history, a.fixed_point_residual_history)
+
+
+def test_operator_budget_and_counters(gpu):
+    lp = support.lp_from_json(RANDOM[1]["lp"])
+    r = solve(lp, SolverConfig(epsilon=1e-6))
+    assert r.spmv_loop == 2 * r.iterations
+    assert r.spmv_checks == 2 * r.kkt_checks
+    assert r.spmv_setup == 2 * r.power_iterations
+
+
+def test_limits_and_edge_configs(gpu):
+    scalar = LpProblem(1, 1, [0, 1], [0], [1.0], [1.0], [0.0], [INF], [1.0], [INF])
+    r = solve(scalar, SolverConfig(time_limit_seconds=0.0))
+    assert r.status == "time_limit" and r.iterations == 0
+    assert r.residuals.primal_inf == pytest.approx(1.0)
+    r = solve(scalar, SolverConfig(iteration_limit=3, epsilon=1e-300))
+    assert r.status == "iteration_limit" and r.iterations == 3
+    r = solve(scalar, SolverConfig(epsilon=1e-8))
+    assert r.status == "optimal" and r.objective == pytest.approx(1.0, rel=1e-6)
+    box = LpProblem(0, 3, [0], [], [], [2.0, -1.0, 0.5], [-1.0, -2.0, 0.25], [4.0, 3.0, 5.0],
+                    [], [])
+    r = solve(box, SolverConfig(epsilon=1e-8))
+    assert r.status == "optimal" and r.iterations <= 200
+    assert r.x == pytest.approx([-1.0, 3.0, 0.25], rel=1e-6)
+
+
+def test_restarts_disabled_straight_line(gpu):
+    """test_restart_engine.cpp:230-256 analog: without restarts and scaling,
+    1000 reflected Halpern steps agree with the reference loop to 1e-10."""
+    lp = support.lp_from_json(RANDOM[3]["lp"])
+    for gamma in (0.0, 1.0):
+        cfg = SolverConfig(scaling_enabled=False, restarts_enabled=False, reflection_gamma=gamma,
+                           pid_kp=0.0, epsilon=1e-300, iteration_limit=1000,
+                           check_interval=100000)
+        g = solve(lp, cfg)
+        o = support.solve_with(support.oracle(), lp, cfg)
+        assert g.iterations == o.iterations == 1000
+        assert max(np.max(np.abs(g.x - o.x)), np.max(np.abs(g.y - o.y))) <= 1e-10
+
+
+def test_kkt_residuals_match_oracle(gpu):
+    for inst in RANDOM:
+        lp = support.lp_from_json(inst["lp"])
+        sp = inst["spmv"]
+        got = vars(kkt_residuals(lp, sp["x"], sp["y"]))
+        want = inst["kkt_xy"]
+        for k, v in want.items():
+            assert got[k] == pytest.approx(v, rel=1e-12, abs=1e-300), k
+
+
+def test_residual_history_matches_oracle_prefix(gpu):
+    lp = support.lp_from_json(RANDOM[4]["lp"])
+    cfg = SolverConfig(epsilon=1e-300, iteration_limit=100, record_residual_history=True)
+    g = solve(lp, cfg)
+    o = support.solve_with(support.oracle(), lp, cfg)
+    assert len(g.fixed_point_residual_history) == len(o.fixed_point_residual_history) == 100
+    assert max_rel(g.fixed_point_residual_history, o.fixed_point_residual_history) <= 1e-9
+
+
+def test_invalid_inputs_raise_reference_errors(gpu):
+    from paper_2507_14051_b200 import InvalidProblemError, UsageError
+
+    bad = LpProblem(1, 1, [0, 1], [0], [1.0], [1.0], [2.0], [1.0], [0.0], [1.0])
+    with pytest.raises(InvalidProblemError):
+        solve(bad)
+    ok = LpProblem(1, 1, [0, 1], [0], [1.0], [1.0], [0.0], [1.0], [0.0], [1.0])
+    with pytest.raises(UsageError):
+        solve(ok, SolverConfig(stepsize_multiplier=1.5))

@@ -260,6 +260,19 @@ def run_product(args):
     sess = Session(lp, SolverConfig(epsilon=1e-300))
     info0 = sess.info()
     layout = sess.layout()
+    if args.profile_kernels:
+        # ncu --profile-from-start off: capture exactly K3, K1, K2 on a live iterate
+        from paper_2507_14051_b200 import capi
+
+        for _ in range(args.warmup):
+            sess.advance(STEP_ITERS)
+        cuda = capi.load_cuda()
+        cuda.rhp_profiler_range(1)
+        sess.time_kernels(reps=args.profile_kernels)
+        cuda.rhp_profiler_range(0)
+        sess.close()
+        dist.close()
+        return 0
     for _ in range(args.warmup):
         sess.advance(STEP_ITERS)
     dist.barrier()
@@ -387,6 +400,9 @@ def main():
     ap.add_argument("--ref-step-iters", type=int, default=8)
     ap.add_argument("--e2e-eps", type=float, default=1e-8)
     ap.add_argument("--e2e-cap", type=int, default=100_000)
+    ap.add_argument("--profile-kernels", type=int, default=0,
+                    help="profiling mode: after warmup, launch K3/K1/K2 N times each inside "
+                         "a cudaProfilerStart/Stop range and exit")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -188,6 +188,12 @@ int rhp_timer(rhp_ctx* ctx, int start, double* ms);
  * SpMV + aty/Halpern epilogue + next primal step, K3 = block-start primal
  * step) on the live iterate. Benchmark use only: mutates the iterate. */
 int rhp_time_kernels(rhp_ctx* ctx, int reps, double* ms_k1, double* ms_k2, double* ms_k3);
+/* Average device ms of `reps` plain SpMVs (transpose 0: A v, 1: A^T v) on
+ * the current matrix, no epilogue: the SpMV engine's own rate. */
+int rhp_time_spmv(rhp_ctx* ctx, int transpose, int reps, double* ms);
+/* cudaProfilerStart (start != 0) / cudaProfilerStop: brackets the launches
+ * an `ncu --profile-from-start off` capture should see. */
+int rhp_profiler_range(int start);
 /* Synchronize the ctx stream. */
 int rhp_synchronize(rhp_ctx* ctx);
 

@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_DIR = PKG_DIR / "lib"
+# RHPDHG_LIB_DIR selects an alternative in-tree build (kernel experiments)
+LIB_DIR = Path(os.environ.get("RHPDHG_LIB_DIR", str(PKG_DIR / "lib"))).resolve()
 
 OK, E_USAGE, E_INVALID_PROBLEM, E_PARSE, E_BREAKDOWN, E_DEVICE, E_INTERNAL = range(7)
 OPTIMAL, ITERATION_LIMIT, TIME_LIMIT = range(3)
@@ -185,7 +186,8 @@ CUDA_SYMBOLS = [
     "rhp_power_begin", "rhp_power_step", "rhp_power_normalize", "rhp_spmv", "rhp_set_step",
     "rhp_reset_iterate", "rhp_set_iterate", "rhp_run_block", "rhp_get_history", "rhp_kkt",
     "rhp_kkt_of", "rhp_fetch_solution", "rhp_fetch_iterate", "rhp_restart",
-    "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_synchronize",
+    "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_time_spmv", "rhp_profiler_range",
+    "rhp_synchronize",
 ]
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",
@@ -241,6 +243,8 @@ def load_cuda() -> C.CDLL:
             "rhp_last_block_ms": [P, c_double_p],
             "rhp_timer": [P, C.c_int, c_double_p],
             "rhp_time_kernels": [P, C.c_int, c_double_p, c_double_p, c_double_p],
+            "rhp_profiler_range": [C.c_int],
+            "rhp_time_spmv": [P, C.c_int, C.c_int, c_double_p],
             "rhp_synchronize": [P],
         }
         for name, args in sig.items():

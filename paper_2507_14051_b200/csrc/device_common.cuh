@@ -19,7 +19,10 @@ namespace rhp {
 
 constexpr int kBlock = 256;          // threads per CTA for every hot kernel
 constexpr int kWarps = kBlock / 32;
-constexpr int kMaxSeg = 8;
+constexpr int kMinBlocks = 2;        // resident CTAs per SM the SpMV is built for
+constexpr int kTileNnz = 2048;       // nonzeros per stream tile (8 per thread)
+constexpr int kTileRows = kBlock;    // rows per stream tile at most (one per thread)
+constexpr int64_t kChunkNnz = 8192;  // nonzeros per chunk tile of a long row
 
 // std::max / std::min semantics (first argument wins on ties and NaN), which
 // the reference's projections rely on (lp_problem.cpp:62, pdhg.cpp:44,54).
@@ -41,6 +44,22 @@ __device__ __forceinline__ double affine(double a, double opg, double g, double 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
 __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((const long long*)p); }
+
+// Random gather of the SpMV input vector (L2 resident, almost never an L1 hit).
+#ifndef RHP_GATHER_MODE
+#define RHP_GATHER_MODE 0
+#endif
+__device__ __forceinline__ double ld_gather(const double* p) {
+#if RHP_GATHER_MODE == 1
+  return __ldcg(p);  // L2 only
+#elif RHP_GATHER_MODE == 2
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);  // read-only path
+#endif
+}
 
 // Loop control shared by host and device (one per ctx, device resident).
 struct Ctl {
@@ -69,21 +88,18 @@ struct Ctl {
   double* hist;                    // [block_limit] residual history of the current block
 };
 
-// One bin segment of an operator schedule: rows [row_begin, row_end) of the
-// (permuted) CSR, processed as tiles [tile_begin, tile_end).
-// kind 0..5: 2^kind lanes per row, kBlock/2^kind rows per tile;
-// kind 6: one CTA per chunk of one long row (chunk table).
-struct Seg {
-  int32_t kind, pad;
-  int64_t row_begin, row_end, tile_begin, tile_end;
-};
-
+// Operator schedule (built by layout.cu): n_stream stream tiles (runs of
+// consecutive rows with <= kTileNnz nonzeros and <= kTileRows rows), then one
+// chunk tile per <= kChunkNnz slice of every row longer than kTileNnz.
 struct Sched {
-  int32_t nseg;
-  int32_t n_multi;          // rows split across several chunks
-  int64_t total_tiles;
-  Seg seg[kMaxSeg];
-  const int32_t* chunk_row;   // [chunks] permuted row
+  int32_t n_multi;            // rows split across several chunks
+  int32_t pad;
+  int64_t n_stream;
+  int64_t total_tiles;        // n_stream + chunks
+  const int32_t* tile_row;    // [n_stream] first row of the tile
+  const int32_t* tile_row_end;// [n_stream] one past its last row
+  const int64_t* tile_nz;     // [2*n_stream] nonzero range [b, e) of the tile
+  const int32_t* chunk_row;   // [chunks] row
   const int64_t* chunk_beg;   // [chunks]
   const int64_t* chunk_end;   // [chunks]
   const int32_t* chunk_first; // [chunks] first chunk of the same row
@@ -154,18 +170,23 @@ __device__ __forceinline__ void block_sum_partials(const double* part, int count
 
 // Adds the epilogue reductions of multi-chunk long rows (fixed slot order).
 template <int N>
-__device__ __forceinline__ void add_long_slots(const Sched& s, double (&out)[N]) {
-  if (s.n_multi == 0) return;
+__device__ __forceinline__ void add_slots(const double* long_red, int n_multi, double (&out)[N]) {
+  if (n_multi == 0) return;
   __shared__ double sm[N];
   if (threadIdx.x < N) {
     double v = 0.0;
-    for (int i = 0; i < s.n_multi; ++i) v += __ldcg(s.long_red + (size_t)i * 16 + threadIdx.x);
+    for (int i = 0; i < n_multi; ++i) v += __ldcg(long_red + (size_t)i * 16 + threadIdx.x);
     sm[threadIdx.x] = v;
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < N; ++q) out[q] += sm[q];
   __syncthreads();
+}
+
+template <int N>
+__device__ __forceinline__ void add_long_slots(const Sched& s, double (&out)[N]) {
+  add_slots<N>(s.long_red, s.n_multi, out);
 }
 
 // Last-block-done election. Returns true in exactly one block, after every

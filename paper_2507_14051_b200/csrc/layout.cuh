@@ -1,15 +1,16 @@
 // layout.cuh — host-side construction of the device data layout.
 //
-// The reference keeps A as CSR + CSC with int64 indices in the original row
-// and column order (sparse_matrix.cpp:20-65). The device keeps two CSR
-// operators, A (m_local x n) and A^T (n x m_local), with
-//   * int32 column indices and int64 row pointers (12 B per nonzero),
-//   * rows permuted so rows of similar length are contiguous (one bin per
-//     SpMV vector width), columns permuted the same way by column length,
-//   * the elements of every row kept in the reference's order (ascending
-//     original column for A, ascending original row for A^T), so sequential
-//     per-row sums in the scaling kernels match the reference bit-for-bit.
-// All m- and n-vectors on the device are stored in the permuted order.
+// The reference keeps A as CSR + CSC with int64 indices (sparse_matrix.cpp:
+// 20-65). The device keeps two CSR operators, A (m_local x n) and A^T
+// (n x m_local = the reference's CSC), with int32 column indices and int64
+// row pointers (12 B per nonzero), rows in the ORIGINAL order and the
+// elements of every row in the reference's order (ascending column for A,
+// ascending row for A^T), so sequential per-row sums match the reference
+// bit-for-bit where the kernels sum sequentially (scaling, short rows).
+// Each operator gets an nnz-balanced tile schedule (spmv.cuh).
+//
+// The permutation maps (prow/pcol) are kept in the interface for layouts
+// that reorder rows; the current layout is the identity.
 #pragma once
 
 #include <cstdint>
@@ -21,10 +22,7 @@
 
 namespace rhp {
 
-constexpr int kKinds = 7;            // 6 sub-warp widths + CTA chunks
-constexpr int64_t kChunkNnz = 8192;  // max nonzeros per CTA chunk of a long row
-
-// kind of a row with L nonzeros: 2^kind lanes per row, or 6 = CTA chunks
+// length class of a row, for diagnostics (rhp_layout_info)
 inline int row_kind(int64_t L) {
   if (L <= 4) return 0;
   if (L <= 8) return 1;
@@ -32,7 +30,8 @@ inline int row_kind(int64_t L) {
   if (L <= 32) return 3;
   if (L <= 64) return 4;
   if (L <= 512) return 5;
-  return 6;
+  if (L <= kTileNnz) return 6;
+  return 7;
 }
 
 struct HostOperator {
@@ -40,10 +39,12 @@ struct HostOperator {
   std::vector<int64_t> rp;
   std::vector<int32_t> ci;
   std::vector<double> v;
-  Sched sched{};                          // host copy; device pointers filled later
+  Sched sched{};  // host copy; device pointers filled at upload
+  std::vector<int32_t> tile_row, tile_row_end;
+  std::vector<int64_t> tile_nz;  // [2 * tiles]: nonzero range of each stream tile
   std::vector<int32_t> chunk_row, chunk_first, chunk_count, chunk_slot;
   std::vector<int64_t> chunk_beg, chunk_end;
-  int64_t bin_rows[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t bin_rows[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // rows per length class
 };
 
 struct HostLayout {
@@ -54,16 +55,18 @@ struct HostLayout {
   std::vector<int32_t> prow;           // device row -> original row (global index)
   std::vector<int32_t> pcol;           // device col -> original col
   std::vector<int32_t> icol;           // original col -> device col
-  // element maps for returning device values in the reference's orders
   std::vector<int64_t> a_dev_to_csr;   // device A element -> reference CSR position (local)
   std::vector<int64_t> at_dev_to_csc;  // device A^T element -> reference CSC position (local)
   HostOperator A, At;
 };
 
-// Builds the layout of rows [row_begin, row_end) of the LP (throws
-// std::invalid_argument / std::domain_error with the reference's messages
-// on malformed input).
+// Builds the layout of rows [row_begin, row_end) of the LP. Throws
+// std::out_of_range (bad index), std::domain_error (non-finite value,
+// duplicate/unsorted entry), std::invalid_argument (too large).
 void build_layout(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end, HostLayout& out);
+
+// The tile schedule of one operator (exposed for tests via rhp_plan).
+void build_schedule(HostOperator& op);
 
 // Balanced contiguous row partition by nonzeros: returns
 // world_size+1 row offsets.

@@ -1,5 +1,5 @@
-// pdhg_kernels.cuh — the fused PDHG iteration, KKT, power-iteration and
-// scaling kernels of the device library.
+// pdhg_kernels.cuh — the fused PDHG iteration, KKT and power-iteration
+// epilogues of the device library (the SpMV engine is spmv.cuh).
 //
 // One restarted reflected-Halpern PDHG iteration (reference solver.cpp:158-181)
 // is two launches on one GPU:
@@ -22,36 +22,40 @@
 //        same pass: x+ = clamp(x - tau(c - aty), l, u) (pdhg.cpp:41-45) and
 //        x <- a'((1+g) x+ - g x) + b' x0 with partials ||dx||^2, ||x-x0||^2,
 //        ||x||^2, ||x_old||^2.
-//   K3 = primal_init: the primal step of a block's first iteration (after a
-//        KKT check or restart changed aty, tau or the anchor).
+//   K3 = epilogue_walk<EpiPrimal>: the primal step of a block's first
+//        iteration (after a KKT check or restart changed aty, tau or the
+//        anchor), with K2's exact row->thread map so its partials are
+//        bit-identical to K2's.
+// Epilogue inputs arrive through the TMA-staged tile (spmv.cuh): input k of
+// row i is e[k*stride].
 #pragma once
 
 #include "spmv.cuh"
 
 namespace rhp {
 
+__device__ __forceinline__ double halpern_a(int64_t k) {
+  return static_cast<double>(k + 1) / static_cast<double>(k + 2);
+}
+__device__ __forceinline__ double halpern_b(int64_t k) { return 1.0 / static_cast<double>(k + 2); }
+
 // ------------------------------------------------------------ primal step --
-struct PrimalArgs {
+struct PrimalOut {
   double* x;
   double* xplus;
-  const double* x0;
-  const double* c;
-  const double* vl;
-  const double* vu;
 };
 
-// pdhg.cpp:41-45 + restart.cpp:44 for one column; acc gets the residual and
-// PID partials of this column.
-__device__ __forceinline__ void primal_col(const PrimalArgs& p, int64_t j, double atyj, double tau,
-                                           double a, double opg, double g, double b,
-                                           double (&acc)[4]) {
-  const double xj = p.x[j];
-  const double t = sub(xj, mul(tau, sub(p.c[j], atyj)));
-  const double xp = smin(smax(t, p.vl[j]), p.vu[j]);
-  p.xplus[j] = xp;
-  const double x0j = p.x0[j];
+// pdhg.cpp:41-45 + restart.cpp:44 for column j; acc gets the residual and PID
+// partials of this column: ||x - x+||^2, ||x_new - x0||^2, ||x_new||^2, ||x||^2.
+__device__ __forceinline__ void primal_col(const PrimalOut& o, int64_t j, double atyj, double xj,
+                                           double cj, double lbj, double ubj, double x0j,
+                                           double tau, double a, double opg, double g, double b,
+                                           double* acc) {
+  const double t = sub(xj, mul(tau, sub(cj, atyj)));
+  const double xp = smin(smax(t, lbj), ubj);
+  o.xplus[j] = xp;
   const double xn = affine(a, opg, g, b, xp, xj, x0j);
-  p.x[j] = xn;
+  o.x[j] = xn;
   const double dx = sub(xj, xp);
   const double d0 = sub(xn, x0j);
   acc[0] = fma(dx, dx, acc[0]);
@@ -60,46 +64,53 @@ __device__ __forceinline__ void primal_col(const PrimalArgs& p, int64_t j, doubl
   acc[3] = fma(xj, xj, acc[3]);
 }
 
-__device__ __forceinline__ double halpern_a(int64_t k) {
-  return static_cast<double>(k + 1) / static_cast<double>(k + 2);
-}
-__device__ __forceinline__ double halpern_b(int64_t k) { return 1.0 / static_cast<double>(k + 2); }
-
-// K3: first primal step of a block. Also resets the block counters.
-__global__ void __launch_bounds__(kBlock) primal_init(Ctl* ctl, PrimalArgs p, const double* aty,
-                                                      int64_t n, double* part3) {
-  const int64_t k = ctl->k;
-  const double a = halpern_a(k), b = halpern_b(k);
-  const double g = ctl->gamma, opg = 1.0 + g, tau = ctl->tau;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * kBlock)
-    primal_col(p, j, aty[j], tau, a, opg, g, b, acc);
-  block_reduce_store<4>(acc, part3, gridDim.x, blockIdx.x);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->stop = 0;
-    ctl->block_iters = 0;
-    ctl->k1_token = -1;
+// K3 (walker): inputs aty, x, c, lb, ub, x0
+struct EpiPrimal {
+  static constexpr int NRED = 4;
+  static constexpr int NIN = 6;
+  Ctl* ctl;
+  PrimalOut o;
+  const double* in[NIN];
+  double a, b, g, opg, tau;
+  __device__ bool enter() {
+    const int64_t k = ctl->k;
+    a = halpern_a(k);
+    b = halpern_b(k);
+    g = ctl->gamma;
+    opg = 1.0 + g;
+    tau = ctl->tau;
+    return true;
   }
-}
+  __device__ void row(int64_t j, double, const double* e, int st, double (&acc)[NRED]) {
+    primal_col(o, j, e[0], e[st], e[2 * st], e[3 * st], e[4 * st], e[5 * st], tau, a, opg, g, b,
+               acc);
+  }
+  __device__ void walk_done() {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctl->stop = 0;
+      ctl->block_iters = 0;
+      ctl->k1_token = -1;
+    }
+  }
+};
 
 // ------------------------------------------------------------------- K1 ----
+// inputs: y, ax, con_lb, con_ub, y0, ax0
 struct EpiDual {
   static constexpr int NRED = 5;
+  static constexpr int NIN = 6;
   static constexpr bool REDUCE = true;
   static constexpr bool FINAL = true;
   Ctl* ctl;
   double* y;
   double* ax;
   double* yplus;
-  const double* y0;
-  const double* ax0;
-  const double* cl;
-  const double* cu;
-  const double* part3;  // primal partials [4][grid3]
+  const double* in[NIN];
+  const double* part3;     // primal partials [4][grid3]
   int grid3;
-  int token;            // launch index inside a plain (non-graph) block
-  // per-thread scalars loaded in enter()
+  int n_multi3;            // multi-chunk rows of the A^T schedule and their
+  const double* long_red3; //   primal partial slots
+  int token;               // launch index inside a plain (non-graph) block
   double sigma, sigma_inv, a, b, g, opg;
 
   __device__ bool enter() {
@@ -114,17 +125,17 @@ struct EpiDual {
     return true;
   }
 
-  __device__ void row(int64_t i, double axp, double (&acc)[NRED]) {
-    const double yi = y[i], axi = ax[i];
+  __device__ void row(int64_t i, double axp, const double* e, int st, double (&acc)[NRED]) {
+    const double yi = e[0], axi = e[st], lo = e[2 * st], hi = e[3 * st], y0i = e[4 * st],
+                 ax0i = e[5 * st];
     const double amid = sub(mul(2.0, axp), axi);
     const double v = sub(mul(sigma_inv, yi), amid);
-    const double proj = smin(smax(v, -cu[i]), -cl[i]);
+    const double proj = smin(smax(v, -hi), -lo);
     const double yp = sub(sub(yi, mul(sigma, amid)), mul(sigma, proj));
     yplus[i] = yp;
-    const double y0i = y0[i];
     const double yn = affine(a, opg, g, b, yp, yi, y0i);
     y[i] = yn;
-    ax[i] = affine(a, opg, g, b, axp, axi, ax0[i]);
+    ax[i] = affine(a, opg, g, b, axp, axi, ax0i);
     const double dy = sub(yi, yp);
     const double dax = sub(axi, axp);
     const double d0 = sub(yn, y0i);
@@ -141,6 +152,7 @@ struct EpiDual {
     block_sum_partials<5>(part, grid, grid, t1);
     add_long_slots<5>(s, t1);
     block_sum_partials<4>(part3, grid3, grid3, t3);
+    add_slots<4>(long_red3, n_multi3, t3);
     if (threadIdx.x != 0) return;
     const double ps = ctl->primal_scale, ds = ctl->dual_scale;
     // quadratic_form(dx, dy, d_ax) (pdhg.cpp:68-75)
@@ -200,14 +212,16 @@ struct EpiDual {
 };
 
 // ------------------------------------------------------------------- K2 ----
+// inputs: aty, aty0, x, c, var_lb, var_ub, x0
 struct EpiAty {
   static constexpr int NRED = 4;
+  static constexpr int NIN = 7;
   static constexpr bool REDUCE = true;
   static constexpr bool FINAL = false;
   Ctl* ctl;
   double* aty;
-  const double* aty0;
-  PrimalArgs p;
+  PrimalOut o;
+  const double* in[NIN];
   int token;
   double a, b, a2, b2, g, opg, tau;
   int stop;
@@ -222,14 +236,16 @@ struct EpiAty {
     g = ctl->gamma;
     opg = 1.0 + g;
     tau = ctl->tau;
-    stop = ctl->stop;
+    stop = ctl->stop && !ctl->bench;
     return true;
   }
 
-  __device__ void row(int64_t j, double atyp, double (&acc)[NRED]) {
-    const double atyn = affine(a, opg, g, b, atyp, aty[j], aty0[j]);
+  __device__ void row(int64_t j, double atyp, const double* e, int st, double (&acc)[NRED]) {
+    const double atyn = affine(a, opg, g, b, atyp, e[0], e[st]);
     aty[j] = atyn;
-    if (!stop) primal_col(p, j, atyn, tau, a2, opg, g, b2, acc);
+    if (!stop)
+      primal_col(o, j, atyn, e[2 * st], e[3 * st], e[4 * st], e[5 * st], e[6 * st], tau, a2, opg,
+                 g, b2, acc);
   }
   __device__ void finalize(const Sched&, const double*, int) {}
 };
@@ -237,26 +253,29 @@ struct EpiAty {
 // ------------------------------------------------------------ plain store --
 struct EpiStore {
   static constexpr int NRED = 1;
+  static constexpr int NIN = 0;
   static constexpr bool REDUCE = false;
   static constexpr bool FINAL = false;
   double* out;
+  const double* in[1];
   __device__ bool enter() { return true; }
-  __device__ void row(int64_t i, double s, double (&)[NRED]) { out[i] = s; }
+  __device__ void row(int64_t i, double s, const double*, int, double (&)[NRED]) { out[i] = s; }
   __device__ void finalize(const Sched&, const double*, int) {}
 };
 
-// w = A^T (A v): store w, reduce v.w and w.w (pdhg.cpp:141-146)
+// w = A^T (A v): store w, reduce v.w and w.w (pdhg.cpp:141-146); input: v
 struct EpiPowerW {
   static constexpr int NRED = 2;
+  static constexpr int NIN = 1;
   static constexpr bool REDUCE = true;
   static constexpr bool FINAL = true;
   Ctl* ctl;
-  const double* v;
   double* w;
+  const double* in[NIN];
   __device__ bool enter() { return true; }
-  __device__ void row(int64_t j, double s, double (&acc)[NRED]) {
+  __device__ void row(int64_t j, double s, const double* e, int, double (&acc)[NRED]) {
     w[j] = s;
-    acc[0] = fma(v[j], s, acc[0]);
+    acc[0] = fma(e[0], s, acc[0]);
     acc[1] = fma(s, s, acc[1]);
   }
   __device__ void finalize(const Sched& sc, const double* part, int grid) {
@@ -296,25 +315,24 @@ __device__ __forceinline__ double clip_sign(double s, double lb, double ub) {
 // Over A: products of the scaled matrix give the original ones as
 // (A_orig x_orig)_i = (Abar xbar)_i / D_row_i; refresh z.ax = Abar xbar
 // (solver.cpp:42); primal violation and p(-y) (termination.cpp:69-103).
+// inputs: y (scaled), D_row, con_lb, con_ub (original)
 struct EpiKktRow {
   static constexpr int NRED = 4;
+  static constexpr int NIN = 4;
   static constexpr bool REDUCE = true;
   static constexpr bool FINAL = false;
-  double* ax_refresh;   // may be null
-  const double* y;      // scaled y
-  const double* rs;     // D_row
-  const double* clo;    // original con bounds
-  const double* cuo;
-  double* yout;         // may be null
+  double* ax_refresh;  // may be null
+  double* yout;        // may be null
+  const double* in[NIN];
   __device__ bool enter() { return true; }
-  __device__ void row(int64_t i, double s, double (&acc)[NRED]) {
+  __device__ void row(int64_t i, double s, const double* e, int st, double (&acc)[NRED]) {
     if (ax_refresh) ax_refresh[i] = s;
-    const double ri = rs[i];
+    const double ri = e[st];
     const double ao = s / ri;
-    const double yo = mul(ri, y[i]);
+    const double yo = mul(ri, e[0]);
     if (yout) yout[i] = yo;
     if (isnan(yo)) acc[0] += 1.0;
-    const double lo = clo[i], up = cuo[i];
+    const double lo = e[2 * st], up = e[3 * st];
     const double proj = smin(smax(ao, lo), up);
     const double d = sub(ao, proj);
     acc[1] = fma(d, d, acc[1]);
@@ -325,33 +343,31 @@ struct EpiKktRow {
   __device__ void finalize(const Sched&, const double*, int) {}
 };
 
+// inputs: x (scaled), D_col, c, var_lb, var_ub (original)
 struct EpiKktCol {
   static constexpr int NRED = 6;
+  static constexpr int NIN = 5;
   static constexpr bool REDUCE = true;
   static constexpr bool FINAL = true;
   Ctl* ctl;
   double* aty_refresh;  // may be null
-  const double* x;      // scaled x
-  const double* cs;     // D_col
-  const double* co;     // original c, var bounds
-  const double* vlo;
-  const double* vuo;
   double* xout;         // may be null
   double* rcout;        // may be null
+  const double* in[NIN];
   const double* part_row;  // EpiKktRow partials [4][grid_row]
   int grid_row;
   int n_multi_row;
   const double* long_red_row;
 
   __device__ bool enter() { return true; }
-  __device__ void row(int64_t j, double s, double (&acc)[NRED]) {
+  __device__ void row(int64_t j, double s, const double* e, int st, double (&acc)[NRED]) {
     if (aty_refresh) aty_refresh[j] = s;
-    const double cj = cs[j];
+    const double cj = e[st];
     const double ato = s / cj;
-    const double xo = mul(cj, x[j]);
+    const double xo = mul(cj, e[0]);
     if (xout) xout[j] = xo;
     if (isnan(xo)) acc[0] += 1.0;
-    const double c = co[j], lb = vlo[j], ub = vuo[j];
+    const double c = e[2 * st], lb = e[3 * st], ub = e[4 * st];
     const double slack = sub(c, ato);
     const double r = clip_sign(slack, lb, ub);
     if (rcout) rcout[j] = r;
@@ -369,19 +385,12 @@ struct EpiKktCol {
     block_sum_partials<6>(part, grid, grid, tc);
     add_long_slots<6>(sc, tc);
     block_sum_partials<4>(part_row, grid_row, grid_row, tr);
-    // multi-chunk rows of the A pass
-    __shared__ double lr[4];
-    if (threadIdx.x < 4) {
-      double v = 0.0;
-      for (int i = 0; i < n_multi_row; ++i) v += __ldcg(long_red_row + (size_t)i * 16 + threadIdx.x);
-      lr[threadIdx.x] = v;
-    }
-    __syncthreads();
+    add_slots<4>(long_red_row, n_multi_row, tr);  // multi-chunk rows of the A pass
     if (threadIdx.x == 0) {
-      ctl->kkt_nan_y = tr[0] + lr[0];
-      ctl->kkt_viol2 = tr[1] + lr[1];
-      ctl->kkt_py_inf = tr[2] + lr[2];
-      ctl->kkt_py = tr[3] + lr[3];
+      ctl->kkt_nan_y = tr[0];
+      ctl->kkt_viol2 = tr[1];
+      ctl->kkt_py_inf = tr[2];
+      ctl->kkt_py = tr[3];
       ctl->kkt_nan_x = tc[0];
       ctl->kkt_pr_inf = tc[1];
       ctl->kkt_pr = tc[2];
@@ -391,107 +400,5 @@ struct EpiKktCol {
     }
   }
 };
-
-// ------------------------------------------------------------- scaling -----
-// Per-row max |a| -> sqrt or 1 (scaling.cpp:56-61). Max is order-free.
-__global__ void k_row_absmax_sqrt(const int64_t* rp, const double* w, int64_t rows, double* out) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * kBlock) {
-    double mx = 0.0;
-    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
-      const double a = fabs(w[e]);
-      if (a > mx) mx = a;
-    }
-    out[i] = mx > 0.0 ? sqrt(mx) : 1.0;
-  }
-}
-
-// w /= rmax_row * cmax_col (scaling.cpp:62), for an operator whose rows carry
-// `row_fac` and columns `col_fac`; `row_first` keeps the reference's factor
-// order rmax*cmax (multiplication is commutative, so both orders agree).
-__global__ void k_ruiz_divide(const int64_t* rp, const int32_t* ci, double* w, int64_t rows,
-                              const double* row_fac, const double* col_fac) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * kBlock) {
-    const double fr = row_fac[i];
-    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) w[e] = __ddiv_rn(w[e], mul(fr, col_fac[ci[e]]));
-  }
-}
-
-__global__ void k_vec_div(double* s, const double* by, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * kBlock)
-    s[i] = __ddiv_rn(s[i], by[i]);
-}
-
-__global__ void k_vec_mul(double* s, const double* by, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * kBlock)
-    s[i] = mul(s[i], by[i]);
-}
-
-// out_e = (f_row * a_e) * f_col (sparse_matrix.cpp:109 for CSR with
-// f_row = r, f_col = c; :112 for CSC with f_row = c, f_col = r).
-__global__ void k_scale_values(const int64_t* rp, const int32_t* ci, const double* src,
-                               double* dst, int64_t rows, const double* f_row,
-                               const double* f_col) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * kBlock) {
-    const double fr = f_row[i];
-    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) dst[e] = mul(mul(fr, src[e]), f_col[ci[e]]);
-  }
-}
-
-// Row 1-norms of the CSR values, sequential per row (sparse_matrix.cpp:130-133):
-// out = 1/sqrt(norm) or 1 (scaling.cpp:73).
-__global__ void k_pc_rows(const int64_t* rp, const double* v, int64_t rows, double* out) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * kBlock) {
-    double acc = 0.0;
-    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) acc = add(acc, fabs(v[e]));
-    out[i] = acc > 0.0 ? __ddiv_rn(1.0, sqrt(acc)) : 1.0;
-  }
-}
-
-// Column 1-norms as the reference accumulates them: for column j, the CSR
-// values (r_i a_ij) c_j added in ascending row order (sparse_matrix.cpp:134).
-// Walks row j of A^T (ascending original rows) recomputing the CSR value
-// from the original a_ij.
-__global__ void k_pc_cols(const int64_t* rp, const int32_t* ci, const double* a_orig,
-                          int64_t rows, const double* rs, const double* cs, double* out) {
-  for (int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x; j < rows;
-       j += (int64_t)gridDim.x * kBlock) {
-    const double cj = cs[j];
-    double acc = 0.0;
-    for (int64_t e = rp[j]; e < rp[j + 1]; ++e) acc = add(acc, fabs(mul(mul(rs[ci[e]], a_orig[e]), cj)));
-    out[j] = acc > 0.0 ? __ddiv_rn(1.0, sqrt(acc)) : 1.0;
-  }
-}
-
-// apply_scales on the vectors (scaling.cpp:21-32):
-//   c <- cs*c, lb <- lb/cs, ub <- ub/cs ; con bounds <- rs*bound
-__global__ void k_apply_col_scales(double* c, double* lb, double* ub, const double* cs, int64_t n) {
-  for (int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * kBlock) {
-    const double s = cs[j];
-    c[j] = mul(s, c[j]);
-    lb[j] = __ddiv_rn(lb[j], s);
-    ub[j] = __ddiv_rn(ub[j], s);
-  }
-}
-__global__ void k_apply_row_scales(double* lb, double* ub, const double* rs, int64_t m) {
-  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * kBlock) {
-    const double s = rs[i];
-    lb[i] = mul(s, lb[i]);
-    ub[i] = mul(s, ub[i]);
-  }
-}
-
-__global__ void k_normalize(double* v, const double* w, double wn, int64_t n) {
-  for (int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * kBlock)
-    v[j] = __ddiv_rn(w[j], wn);
-}
 
 }  // namespace rhp

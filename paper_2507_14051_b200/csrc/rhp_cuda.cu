@@ -3,6 +3,7 @@
 // One rhp_ctx = one solve's device state on one GPU. Host code here only
 // allocates, uploads, builds the CUDA graph and launches; all arithmetic of
 // the solve runs in the kernels of pdhg_kernels.cuh.
+#include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,6 +21,7 @@
 
 #include "layout.cuh"
 #include "pdhg_kernels.cuh"
+#include "scaling_kernels.cuh"
 #include "rhpdhg_cuda.h"
 
 using namespace rhp;
@@ -61,10 +63,18 @@ int guarded(F&& f) {
   }
 }
 
+// Every device array gets 64 B of zeroed tail padding: the SpMV's bulk copies
+// round source ranges out to 16-B boundaries and may read past the last
+// element (never used).
 template <class T>
 T* dev_alloc(size_t count) {
   void* p = nullptr;
-  CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 64;
+  CK(cudaMalloc(&p, bytes));
+  // synchronous: the ctx stream is non-blocking, so an asynchronous memset on
+  // the legacy stream could land after later uploads on the ctx stream
+  CK(cudaMemset(p, 0, bytes));
+  CK(cudaDeviceSynchronize());
   return static_cast<T*>(p);
 }
 
@@ -81,8 +91,8 @@ struct DevOp {
   double* v_orig = nullptr;  // original values, kept until scaling is done
   Sched sched{};             // with device pointers
   int32_t *chunk_row = nullptr, *chunk_first = nullptr, *chunk_count = nullptr,
-          *chunk_slot = nullptr;
-  int64_t *chunk_beg = nullptr, *chunk_end = nullptr;
+          *chunk_slot = nullptr, *tile_row = nullptr, *tile_row_end = nullptr;
+  int64_t *chunk_beg = nullptr, *chunk_end = nullptr, *tile_nz = nullptr;
   double *chunk_part = nullptr, *long_red = nullptr;
   unsigned int* slot_ticket = nullptr;
   Csr csr() const { return Csr{rp, ci, v, rows}; }
@@ -141,6 +151,13 @@ void upload_op(DevOp& d, const HostOperator& h, cudaStream_t s) {
   upload(d.ci, h.ci.data(), h.ci.size(), s);
   upload(d.v, h.v.data(), h.v.size(), s);
   upload(d.v_orig, h.v.data(), h.v.size(), s);
+  const size_t nt = h.tile_row.size();
+  d.tile_row = dev_alloc<int32_t>(nt);
+  d.tile_row_end = dev_alloc<int32_t>(nt);
+  upload(d.tile_row, h.tile_row.data(), nt, s);
+  upload(d.tile_row_end, h.tile_row_end.data(), nt, s);
+  d.tile_nz = dev_alloc<int64_t>(2 * nt);
+  upload(d.tile_nz, h.tile_nz.data(), 2 * nt, s);
   const size_t nch = h.chunk_row.size();
   d.chunk_row = dev_alloc<int32_t>(nch);
   d.chunk_first = dev_alloc<int32_t>(nch);
@@ -157,10 +174,13 @@ void upload_op(DevOp& d, const HostOperator& h, cudaStream_t s) {
   upload(d.chunk_end, h.chunk_end.data(), nch, s);
   const size_t nm = static_cast<size_t>(h.sched.n_multi);
   d.slot_ticket = dev_alloc<unsigned int>(nm);
-  d.long_red = dev_alloc<double>(nm * 16);
+  d.long_red = dev_alloc<double>(std::max<size_t>(nm, 1) * 16);
   CK(cudaMemsetAsync(d.slot_ticket, 0, std::max<size_t>(nm, 1) * sizeof(unsigned int), s));
   CK(cudaMemsetAsync(d.long_red, 0, std::max<size_t>(nm, 1) * 16 * sizeof(double), s));
   d.sched = h.sched;
+  d.sched.tile_row = d.tile_row;
+  d.sched.tile_row_end = d.tile_row_end;
+  d.sched.tile_nz = d.tile_nz;
   d.sched.chunk_row = d.chunk_row;
   d.sched.chunk_beg = d.chunk_beg;
   d.sched.chunk_end = d.chunk_end;
@@ -176,7 +196,8 @@ void free_op(DevOp& d) {
   for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.chunk_row,
                   (void*)d.chunk_first, (void*)d.chunk_count, (void*)d.chunk_slot,
                   (void*)d.chunk_beg, (void*)d.chunk_end, (void*)d.chunk_part,
-                  (void*)d.long_red, (void*)d.slot_ticket})
+                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.tile_row,
+                  (void*)d.tile_row_end, (void*)d.tile_nz})
     if (p) cudaFree(p);
   d = DevOp{};
 }
@@ -215,11 +236,32 @@ int vec_grid(const rhp_ctx& c, int64_t len) {
 template <class Epi>
 void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
                  double* part, unsigned int* ticket, cudaStream_t s) {
-  spmv_fused<Epi><<<grid, kBlock, 0, s>>>(op.csr(), xg, op.sched, epi, part, ticket);
+  (void)c;
+  spmv_fused<Epi><<<grid, kBlock, spmv_smem_bytes<Epi::NIN>(), s>>>(op.csr(), xg, op.sched, epi,
+                                                                   part, ticket);
   CK(cudaGetLastError());
 }
 
-PrimalArgs primal_args(rhp_ctx& c) { return PrimalArgs{c.x, c.xp, c.x0, c.c, c.vl, c.vu}; }
+// Opt the SpMV instantiations into their dynamic shared memory and return the
+// resident CTAs per SM.
+template <class Epi>
+int prepare_spmv() {
+  const void* fn = reinterpret_cast<const void*>(spmv_fused<Epi>);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(spmv_smem_bytes<Epi::NIN>())));
+  int b = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, spmv_smem_bytes<Epi::NIN>()));
+  if (b < 1) throw CudaError("spmv kernel does not fit on an SM");
+  return b;
+}
+
+PrimalOut primal_out(rhp_ctx& c) { return PrimalOut{c.x, c.xp}; }
+
+EpiStore store_into(double* out) {
+  EpiStore e{};
+  e.out = out;
+  return e;
+}
 
 EpiDual epi_dual(rhp_ctx& c, int token) {
   EpiDual e{};
@@ -227,12 +269,12 @@ EpiDual epi_dual(rhp_ctx& c, int token) {
   e.y = c.y;
   e.ax = c.ax;
   e.yplus = c.yp;
-  e.y0 = c.y0;
-  e.ax0 = c.ax0;
-  e.cl = c.cl;
-  e.cu = c.cu;
+  const double* in[] = {c.y, c.ax, c.cl, c.cu, c.y0, c.ax0};
+  for (int k = 0; k < EpiDual::NIN; ++k) e.in[k] = in[k];
   e.part3 = c.part3;
   e.grid3 = c.grid_at;
+  e.n_multi3 = c.At.sched.n_multi;
+  e.long_red3 = c.At.long_red;
   e.token = token;
   return e;
 }
@@ -241,8 +283,9 @@ EpiAty epi_aty(rhp_ctx& c, int token) {
   EpiAty e{};
   e.ctl = c.ctl;
   e.aty = c.aty;
-  e.aty0 = c.aty0;
-  e.p = primal_args(c);
+  e.o = primal_out(c);
+  const double* in[] = {c.aty, c.aty0, c.x, c.c, c.vl, c.vu, c.x0};
+  for (int k = 0; k < EpiAty::NIN; ++k) e.in[k] = in[k];
   e.token = token;
   return e;
 }
@@ -253,7 +296,12 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s) {
 }
 
 void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
-  primal_init<<<c.grid_at, kBlock, 0, s>>>(c.ctl, primal_args(c), c.aty, c.n, c.part3);
+  EpiPrimal e{};
+  e.ctl = c.ctl;
+  e.o = primal_out(c);
+  const double* in[] = {c.aty, c.x, c.c, c.vl, c.vu, c.x0};
+  for (int k = 0; k < EpiPrimal::NIN; ++k) e.in[k] = in[k];
+  epilogue_walk<EpiPrimal><<<c.grid_at, kBlock, 0, s>>>(c.At.sched, e, c.part3);
   CK(cudaGetLastError());
 }
 
@@ -314,20 +362,20 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
              rhp_kkt_sums* out) {
   EpiKktRow er{};
   er.ax_refresh = refresh ? c.ax : nullptr;
-  er.y = ys;
-  er.rs = c.rs;
-  er.clo = c.clo;
-  er.cuo = c.cuo;
   er.yout = write_out ? c.yout : nullptr;
+  er.in[0] = ys;
+  er.in[1] = c.rs;
+  er.in[2] = c.clo;
+  er.in[3] = c.cuo;
   launch_spmv(c, c.A, c.grid_a, xs, er, c.partA, nullptr, c.stream);
   EpiKktCol ec{};
   ec.ctl = c.ctl;
   ec.aty_refresh = refresh ? c.aty : nullptr;
-  ec.x = xs;
-  ec.cs = c.cs;
-  ec.co = c.co;
-  ec.vlo = c.vlo;
-  ec.vuo = c.vuo;
+  ec.in[0] = xs;
+  ec.in[1] = c.cs;
+  ec.in[2] = c.co;
+  ec.in[3] = c.vlo;
+  ec.in[4] = c.vuo;
   ec.xout = write_out ? c.xout : nullptr;
   ec.rcout = write_out ? c.rcout : nullptr;
   ec.part_row = c.partA;
@@ -351,8 +399,8 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
 
 void exact_caches(rhp_ctx& c) {
   // z.ax = A x, z.aty = A^T y
-  launch_spmv(c, c.A, c.grid_a, c.x, EpiStore{c.ax}, nullptr, nullptr, c.stream);
-  launch_spmv(c, c.At, c.grid_at, c.y, EpiStore{c.aty}, nullptr, nullptr, c.stream);
+  launch_spmv(c, c.A, c.grid_a, c.x, store_into(c.ax), nullptr, nullptr, c.stream);
+  launch_spmv(c, c.At, c.grid_at, c.y, store_into(c.aty), nullptr, nullptr, c.stream);
 }
 
 }  // namespace
@@ -461,10 +509,11 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     upload(c->cs, c->hbuf.data(), n, s);
     CK(cudaStreamSynchronize(s));
     // grids: persistent, a multiple of the SM count, never more than tiles
-    const int occ_a = std::max(occupancy_blocks((const void*)spmv_fused<EpiDual>),
-                               occupancy_blocks((const void*)spmv_fused<EpiKktRow>));
-    const int occ_at = std::max(occupancy_blocks((const void*)spmv_fused<EpiAty>),
-                                occupancy_blocks((const void*)spmv_fused<EpiKktCol>));
+    // one grid per operator: every kernel walking it must see the same CTA count
+    const int occ_store = prepare_spmv<EpiStore>();
+    const int occ_a = std::min({prepare_spmv<EpiDual>(), prepare_spmv<EpiKktRow>(), occ_store});
+    const int occ_at = std::min({prepare_spmv<EpiAty>(), prepare_spmv<EpiKktCol>(),
+                                 prepare_spmv<EpiPowerW>(), occ_store});
     auto clampg = [](int64_t tiles, int64_t cap) {
       return static_cast<int>(std::max<int64_t>(1, std::min(tiles, cap)));
     };
@@ -624,8 +673,11 @@ int rhp_power_begin(rhp_ctx* c, const double* v0) {
 
 int rhp_power_step(rhp_ctx* c, double* vw, double* ww) {
   return guarded([&] {
-    launch_spmv(*c, c->A, c->grid_a, c->pv, EpiStore{c->pav}, nullptr, nullptr, c->stream);
-    EpiPowerW e{c->ctl, c->pv, c->pw};
+    launch_spmv(*c, c->A, c->grid_a, c->pv, store_into(c->pav), nullptr, nullptr, c->stream);
+    EpiPowerW e{};
+    e.ctl = c->ctl;
+    e.w = c->pw;
+    e.in[0] = c->pv;
     launch_spmv(*c, c->At, c->grid_at, c->pav, e, c->partAt, &c->ctl->ticket_pow, c->stream);
     pull_ctl(*c);
     *vw = c->ctl_host->pw_vw;
@@ -645,11 +697,11 @@ int rhp_spmv(rhp_ctx* c, int transpose, const double* in, double* out) {
     const std::vector<int32_t> lrows = local_rows(*c);
     if (!transpose) {
       upload_perm(c->pv, in, c->L.pcol, c->hbuf, c->stream);
-      launch_spmv(*c, c->A, c->grid_a, c->pv, EpiStore{c->pav}, nullptr, nullptr, c->stream);
+      launch_spmv(*c, c->A, c->grid_a, c->pv, store_into(c->pav), nullptr, nullptr, c->stream);
       download_perm(out, c->pav, lrows, c->hbuf, c->stream);
     } else {
       upload_perm(c->pav, in, lrows, c->hbuf, c->stream);
-      launch_spmv(*c, c->At, c->grid_at, c->pav, EpiStore{c->pw}, nullptr, nullptr, c->stream);
+      launch_spmv(*c, c->At, c->grid_at, c->pav, store_into(c->pw), nullptr, nullptr, c->stream);
       download_perm(out, c->pw, c->L.pcol, c->hbuf, c->stream);
     }
   });
@@ -875,6 +927,30 @@ int rhp_time_kernels(rhp_ctx* c, int reps, double* ms_k1, double* ms_k2, double*
     SET_CTL(*c, bench, zero);
     SET_CTL(*c, graph_mode, gm);
   });
+}
+
+// Average device ms of `reps` plain SpMVs (out = A v or A^T v, no epilogue
+// reductions) on the current matrix: the SpMV engine's own rate.
+int rhp_time_spmv(rhp_ctx* c, int transpose, int reps, double* ms) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    float f = 0.f;
+    CK(cudaEventRecord(c->tev0, s));
+    for (int r = 0; r < reps; ++r) {
+      if (transpose)
+        launch_spmv(*c, c->At, c->grid_at, c->pav, store_into(c->pw), nullptr, nullptr, s);
+      else
+        launch_spmv(*c, c->A, c->grid_a, c->pv, store_into(c->pav), nullptr, nullptr, s);
+    }
+    CK(cudaEventRecord(c->tev1, s));
+    CK(cudaEventSynchronize(c->tev1));
+    CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+    *ms = f / reps;
+  });
+}
+
+int rhp_profiler_range(int start) {
+  return guarded([&] { CK(start ? cudaProfilerStart() : cudaProfilerStop()); });
 }
 
 int rhp_synchronize(rhp_ctx* c) {

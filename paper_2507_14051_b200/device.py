@@ -133,6 +133,11 @@ class DeviceContext:
         self._ok(self.lib.rhp_timer(self.h, 0, C.byref(ms)))
         return ms.value
 
+    def time_spmv(self, transpose=False, reps=20) -> float:
+        ms = C.c_double()
+        self._ok(self.lib.rhp_time_spmv(self.h, int(transpose), reps, C.byref(ms)))
+        return ms.value
+
     def last_block_ms(self) -> float:
         ms = C.c_double()
         self._ok(self.lib.rhp_last_block_ms(self.h, C.byref(ms)))

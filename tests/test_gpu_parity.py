@@ -112,6 +112,12 @@ def test_first_100_iterates_match_reference(gpu, inst):
     lp = support.lp_from_json(inst["lp"])
     for k, snap in inst["snapshots"].items():
         r = solve(lp, SolverConfig(epsilon=1e-300, iteration_limit=int(k)))
+        if r.status == "optimal" and r.iterations < int(k):
+            # eps=1e-300 can only be met by EXACTLY zero residuals: a tiny LP
+            # whose KKT sums cancel to 0.0 in the device's summation order
+            # stops at that check; the reference (other order) runs on.
+            assert r.residuals.gap_rel == r.residuals.primal_rel == r.residuals.dual_eq == 0.0
+            break
         assert r.iterations == int(k)
         assert max_rel(r.x, snap["x"]) <= 1e-10, k
         assert max_rel(r.y, snap["y"]) <= 1e-10, k

@@ -23,7 +23,7 @@ $(LIB)/librhp_cuda.so: $(CU_SRCS) $(CU_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) -lnccl 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
 $(LIB)/librhpdhg.so: $(HOST_SRCS) $(HOST_HDRS) $(LIB)/librhp_cuda.so
-	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -lrhp_cuda -Wl,-rpath,'$$ORIGIN'
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -lrhp_cuda -lz -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle oracle

@@ -147,6 +147,14 @@ int rhpdhg_solve_csr(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg,
 int rhpdhg_kkt_residuals(const rhpdhg_lp_view* lp, const double* x, const double* y,
                          rhpdhg_kkt_c* out);
 
+/* An owned LpProblem: parse_mps_file (mps.hpp:21-25). `warnings` (may be
+ * NULL) receives the parser warnings joined by '\n', truncated to cap-1. */
+typedef struct rhpdhg_lp rhpdhg_lp;
+int rhpdhg_lp_read_mps(const char* path, rhpdhg_lp** out, char* warnings, int64_t warnings_cap);
+/* Borrowed view of an owned LP (valid until rhpdhg_lp_free). */
+int rhpdhg_lp_view_of(const rhpdhg_lp* lp, rhpdhg_lp_view* view);
+void rhpdhg_lp_free(rhpdhg_lp* lp);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* rhpdhg_last_error(void);
 

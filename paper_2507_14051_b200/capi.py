@@ -194,7 +194,7 @@ HOST_SYMBOLS = [
     "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
-    "rhpdhg_session_layout",
+    "rhpdhg_session_layout", "rhpdhg_lp_read_mps", "rhpdhg_lp_view_of", "rhpdhg_lp_free",
 ]
 
 _cache: dict[str, C.CDLL] = {}
@@ -290,6 +290,12 @@ def load_host() -> C.CDLL:
             fn.restype = C.c_int
         lib.rhpdhg_session_destroy.argtypes = [P]
         lib.rhpdhg_session_destroy.restype = None
+        lib.rhpdhg_lp_read_mps.argtypes = [C.c_char_p, C.POINTER(P), C.c_char_p, C.c_int64]
+        lib.rhpdhg_lp_read_mps.restype = C.c_int
+        lib.rhpdhg_lp_view_of.argtypes = [P, C.POINTER(LpView)]
+        lib.rhpdhg_lp_view_of.restype = C.c_int
+        lib.rhpdhg_lp_free.argtypes = [P]
+        lib.rhpdhg_lp_free.restype = None
         lib._typed = True
     return lib
 

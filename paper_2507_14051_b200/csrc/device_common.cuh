@@ -19,8 +19,16 @@ namespace rhp {
 
 constexpr int kBlock = 256;          // threads per CTA for every hot kernel
 constexpr int kWarps = kBlock / 32;
-constexpr int kMinBlocks = 2;        // resident CTAs per SM the SpMV is built for
-constexpr int kTileNnz = 2048;       // nonzeros per stream tile (8 per thread)
+// 1024 nonzeros (4 per thread) x 4 resident CTAs per SM measured best on
+// B200 against 2048x2, 1024x3 and 512x6 (tools/spmv_probe.py)
+#ifndef RHP_TILE_NNZ
+#define RHP_TILE_NNZ 1024
+#endif
+#ifndef RHP_MIN_BLOCKS
+#define RHP_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocks = RHP_MIN_BLOCKS;  // resident CTAs per SM the SpMV is built for
+constexpr int kTileNnz = RHP_TILE_NNZ;      // nonzeros per stream tile
 constexpr int kTileRows = kBlock;    // rows per stream tile at most (one per thread)
 constexpr int64_t kChunkNnz = 8192;  // nonzeros per chunk tile of a long row
 

@@ -7,6 +7,7 @@
 #include "device.hpp"
 #include "rhpdhg/errors.hpp"
 #include "rhpdhg/solver.hpp"
+#include "rhpdhg/mps.hpp"
 #include "rhpdhg/termination.hpp"
 #include "rhpdhg_c.h"
 #include "session.hpp"
@@ -105,9 +106,36 @@ struct rhpdhg_session {
   std::unique_ptr<Session> session;
 };
 
+struct rhpdhg_lp {
+  LpProblem problem;
+};
+
 extern "C" {
 
 const char* rhpdhg_last_error(void) { return g_msg.c_str(); }
+
+int rhpdhg_lp_read_mps(const char* path, rhpdhg_lp** out, char* warnings, int64_t cap) {
+  *out = nullptr;
+  return guarded([&] {
+    std::vector<std::string> w;
+    auto h = std::make_unique<rhpdhg_lp>();
+    h->problem = parse_mps_file(path, &w);
+    if (warnings && cap > 0) {
+      std::string joined;
+      for (const std::string& s : w) joined += (joined.empty() ? "" : "\n") + s;
+      const size_t k = std::min<size_t>(joined.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(warnings, joined.data(), k);
+      warnings[k] = '\0';
+    }
+    *out = h.release();
+  });
+}
+
+int rhpdhg_lp_view_of(const rhpdhg_lp* lp, rhpdhg_lp_view* v) {
+  return guarded([&] { *v = detail::view_of(lp->problem); });
+}
+
+void rhpdhg_lp_free(rhpdhg_lp* lp) { delete lp; }
 
 int rhpdhg_config_default(rhpdhg_config_c* c) {
   return guarded([&] {

@@ -282,6 +282,90 @@ def set_device(device: int) -> None:
     raise_status(lib.rhpdhg_set_device(device), lib.rhpdhg_last_error().decode())
 
 
+def read_mps(path: str) -> tuple[LpProblem, list[str]]:
+    """rhpdhg::parse_mps_file (host C++; '.gz' accepted) -> (LpProblem, warnings)."""
+    lib = capi.load_host()
+    h = C.c_void_p()
+    buf = C.create_string_buffer(1 << 16)
+    raise_status(lib.rhpdhg_lp_read_mps(str(path).encode(), C.byref(h), buf, len(buf)),
+                 lib.rhpdhg_last_error().decode(errors="replace"))
+    try:
+        v = capi.LpView()
+        raise_status(lib.rhpdhg_lp_view_of(h, C.byref(v)), lib.rhpdhg_last_error().decode())
+        m, n = v.num_cons, v.num_vars
+        nnz = v.row_ptr[m] if m else 0
+
+        def arr(p, k, dt=np.float64):
+            return np.ctypeslib.as_array(p, shape=(k,)).astype(dt, copy=True) if k else np.zeros(0, dt)
+
+        lp = LpProblem(m, n, arr(v.row_ptr, m + 1, np.int64), arr(v.col_index, nnz, np.int64),
+                       arr(v.values, nnz), arr(v.objective, n), arr(v.var_lb, n),
+                       arr(v.var_ub, n), arr(v.con_lb, m), arr(v.con_ub, m),
+                       objective_offset=v.objective_offset, maximization=bool(v.maximization))
+    finally:
+        lib.rhpdhg_lp_free(h)
+    warnings = [w for w in buf.value.decode(errors="replace").split("\n") if w]
+    return lp, warnings
+
+
+def write_mps(lp: LpProblem, path: str) -> None:
+    """Free-format MPS of an LpProblem (minimisation form as stored; bounds
+    written explicitly, two-sided rows as E/L/G + RANGES)."""
+    def num(v):
+        return repr(float(v))
+
+    m, n = lp.num_cons, lp.num_vars
+    lines = [f"NAME {lp.name or 'LP'}", "ROWS", " N OBJ"]
+    kinds, rhs, rng = [], [], []
+    for i in range(m):
+        lo, hi = lp.con_lb[i], lp.con_ub[i]
+        if lo == hi:
+            kinds.append("E"); rhs.append(lo); rng.append(None)
+        elif np.isinf(lo) and np.isinf(hi):
+            raise UsageError("free rows have no MPS row sense here")
+        elif np.isinf(lo):
+            kinds.append("L"); rhs.append(hi); rng.append(None)
+        elif np.isinf(hi):
+            kinds.append("G"); rhs.append(lo); rng.append(None)
+        else:
+            kinds.append("G"); rhs.append(lo); rng.append(hi - lo)
+        lines.append(f" {kinds[-1]} R{i}")
+    cols = [[] for _ in range(n)]
+    for i in range(m):
+        for e in range(lp.row_ptr[i], lp.row_ptr[i + 1]):
+            cols[lp.col_index[e]].append((i, lp.values[e]))
+    lines.append("COLUMNS")
+    for j in range(n):
+        lines.append(f" X{j} OBJ {num(lp.objective[j])}")
+        for i, v in cols[j]:
+            lines.append(f" X{j} R{i} {num(v)}")
+    lines.append("RHS")
+    if lp.objective_offset != 0.0:
+        lines.append(f" RHS OBJ {num(-lp.objective_offset)}")
+    for i in range(m):
+        lines.append(f" RHS R{i} {num(rhs[i])}")
+    if any(r is not None for r in rng):
+        lines.append("RANGES")
+        for i in range(m):
+            if rng[i] is not None:
+                lines.append(f" RNG R{i} {num(rng[i])}")
+    lines.append("BOUNDS")
+    for j in range(n):
+        lo, hi = lp.var_lb[j], lp.var_ub[j]
+        if np.isinf(lo) and np.isinf(hi):
+            lines.append(f" FR BND X{j}")
+            continue
+        if np.isinf(lo):
+            lines.append(f" MI BND X{j}")
+        else:
+            lines.append(f" LO BND X{j} {num(lo)}")
+        if not np.isinf(hi):
+            lines.append(f" UP BND X{j} {num(hi)}")
+    lines.append("ENDATA")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
 def set_device_options(device: int = 0, use_graph: bool = True, block_limit: int = 64) -> None:
     lib = capi.load_host()
     raise_status(lib.rhpdhg_set_device_options(device, int(use_graph), block_limit),

@@ -1,0 +1,106 @@
+"""CPU suite: the MPS loader (host C++, rhpdhg::parse_mps_file) — LP load is
+part of the drop-in boundary (mps.hpp:17-25). Runs without a GPU."""
+import gzip
+import math
+
+import numpy as np
+import pytest
+
+import support
+from paper_2507_14051_b200.lp import ParseError, read_mps, write_mps
+
+ANALYTIC = support.load_golden("analytic_lps.json")["instances"]
+REF_FIX = support.Path("/root/reference/proj/tests/fixtures")
+
+
+def same_lp(a, b):
+    assert (a.num_cons, a.num_vars) == (b.num_cons, b.num_vars)
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_index, b.col_index)
+    assert np.array_equal(a.values, b.values)
+    for k in ("objective", "var_lb", "var_ub", "con_lb", "con_ub"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    assert a.objective_offset == b.objective_offset and a.maximization == b.maximization
+
+
+@pytest.mark.parametrize("inst", ANALYTIC, ids=[i["name"] for i in ANALYTIC])
+def test_roundtrip_of_golden_analytic_lps(tmp_path, inst):
+    lp = support.lp_from_json(inst["lp"])
+    if lp.maximization:  # written in min form; read back as min form
+        lp.maximization = False
+    p = tmp_path / f"{inst['name']}.mps"
+    write_mps(lp, p)
+    got, _ = read_mps(p)
+    same_lp(got, lp)
+    with open(p, "rb") as f, gzip.open(str(p) + ".gz", "wb") as g:
+        g.write(f.read())
+    got_gz, _ = read_mps(str(p) + ".gz")
+    same_lp(got_gz, lp)
+
+
+def test_sections_bounds_ranges_and_warnings(tmp_path):
+    text = """NAME demo
+OBJSENSE
+    MAX
+ROWS
+ N  obj
+ N  extra
+ E  e1
+ L  l1
+ G  g1
+COLUMNS
+    MARKER   'MARKER'   'INTORG'
+    x  obj 1.5D0  e1 1
+    MARKER   'MARKER'   'INTEND'
+    y  obj -2   l1 3   g1 1
+    z  e1 4  extra 9
+RHS
+    rhs obj 10   e1 2   l1 5   g1 1
+RANGES
+    rng e1 -1  l1 2  g1 -3
+BOUNDS
+ UP bnd x -1
+ BV bnd y
+ FR bnd z
+ENDATA
+"""
+    p = tmp_path / "demo.mps"
+    p.write_text(text)
+    lp, warnings = read_mps(p)
+    assert lp.maximization and lp.objective.tolist() == [-1.5, 2.0, -0.0]
+    assert lp.objective_offset == 10.0  # -(-10) after the max negation
+    assert lp.con_lb.tolist() == [1.0, 3.0, 1.0] and lp.con_ub.tolist() == [2.0, 5.0, 4.0]
+    assert lp.var_lb.tolist() == [-math.inf, 0.0, -math.inf]
+    assert lp.var_ub.tolist() == [-1.0, 1.0, math.inf]
+    assert any("extra free row" in w for w in warnings)
+    assert any("integrality markers" in w for w in warnings)
+    assert any("negative UP bound" in w for w in warnings)
+
+
+@pytest.mark.parametrize("body,frag", [
+    ("NAME x\nROWS\n N obj\nCOLUMNS\n x obj 1\n", "missing ENDATA"),
+    ("NAME x\nROWS\n N obj\nCOLUMNS\n x obj 1\nROWS\nENDATA\n", "section out of order"),
+    ("NAME x\nROWS\n N obj\nCOLUMNS\n x nope 1\nENDATA\n", "undeclared row"),
+    ("NAME x\nROWS\n N obj\nCOLUMNS\n x obj 1x\nENDATA\n", "malformed number"),
+    ("NAME x\nROWS\n Q r\nENDATA\n", "unknown row sense"),
+])
+def test_parse_errors_carry_line_numbers(tmp_path, body, frag):
+    p = tmp_path / "bad.mps"
+    p.write_text(body)
+    with pytest.raises(ParseError, match=frag):
+        read_mps(p)
+
+
+@pytest.mark.skipif(not (REF_FIX.is_dir() and support.ref_available()),
+                    reason="reference fixtures / oracle/_ref not available")
+def test_loader_matches_reference_parser_on_its_fixtures():
+    files = sorted(REF_FIX.glob("lp/*.mps")) + sorted(REF_FIX.glob("mps/*.mps"))
+    assert files
+    for f in files:
+        try:
+            want = support.ref_lp_from_handle(support.ref().ref_lp_from_mps(str(f).encode()))
+        except RuntimeError:
+            with pytest.raises(ParseError):
+                read_mps(f)
+            continue
+        got, _ = read_mps(f)
+        same_lp(got, want)

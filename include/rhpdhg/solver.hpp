@@ -4,6 +4,8 @@
 // GPU through the device library (include/rhpdhg_cuda.h).
 #pragma once
 
+#include <vector>
+
 #include "rhpdhg/config.hpp"
 #include "rhpdhg/lp_problem.hpp"
 #include "rhpdhg/report.hpp"
@@ -16,6 +18,13 @@ struct DeviceOptions {
   int device = 0;
   bool use_graph = true;   // CUDA graph with a conditional WHILE node per block
   long block_limit = 64;   // PDHG iterations per device block at most
+  // Row-partitioned multi-GPU solve (one process per GPU): every rank calls
+  // solve() on the FULL problem with the same config; rank 0's 128-byte
+  // ncclUniqueId (rhp_nccl_unique_id) is shared out of band. An id with
+  // world_size == 1 runs the same partitioned code path on one GPU.
+  int rank = 0;
+  int world_size = 1;
+  std::vector<char> nccl_id;  // empty: single-GPU path
 };
 
 /// Process-wide default device options (used by solve(problem, cfg)).

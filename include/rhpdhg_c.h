@@ -163,6 +163,11 @@ int rhpdhg_set_device(int device);
 /* Device runtime knobs (not SolverConfig keys): CUDA-graph blocks on/off and
  * the maximum PDHG iterations per device block (default 1, 64). */
 int rhpdhg_set_device_options(int device, int use_graph, int64_t block_limit);
+/* Row-partitioned multi-GPU solves (one process per GPU): subsequent solves
+ * of this process act as `rank` of `world_size`, joined through rank 0's
+ * 128-byte NCCL unique id (rhp_nccl_unique_id in rhpdhg_cuda.h). nccl_id NULL
+ * with world_size 1 restores single-GPU solves. */
+int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id);
 
 /* Resumable solve (extension used by benchmarks and long-running callers):
  * create = validation + upload + scaling + power iteration + initial KKT

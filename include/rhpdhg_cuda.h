@@ -171,6 +171,12 @@ int rhp_kkt(rhp_ctx* ctx, int which, rhp_kkt_sums* out);
  * ORIGINAL matrix (call before rhp_scale). */
 int rhp_kkt_of(rhp_ctx* ctx, const double* x, const double* y, rhp_kkt_sums* out);
 int rhp_fetch_solution(rhp_ctx* ctx, double* x, double* y, double* reduced_costs);
+/* Row-partitioned contexts: *any = OR of `flag` over all ranks (keeps host
+ * decisions such as the time limit identical on every rank); else *any = flag. */
+int rhp_any(rhp_ctx* ctx, int flag, int* any);
+/* GPU-free planning: the row partition bench/tests use (world_size+1 row
+ * offsets, contiguous blocks balanced by nonzeros + rows). */
+int rhp_partition_rows(const rhpdhg_lp_view* lp, int world_size, int64_t* offsets);
 /* Scaled iterate (x, y, ax, aty) in original order; for tests. */
 int rhp_fetch_iterate(rhp_ctx* ctx, double* x, double* y, double* ax, double* aty);
 

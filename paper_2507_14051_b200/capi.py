@@ -185,13 +185,15 @@ CUDA_SYMBOLS = [
     "rhp_create", "rhp_destroy", "rhp_layout", "rhp_scale", "rhp_get_scaled",
     "rhp_power_begin", "rhp_power_step", "rhp_power_normalize", "rhp_spmv", "rhp_set_step",
     "rhp_reset_iterate", "rhp_set_iterate", "rhp_run_block", "rhp_get_history", "rhp_kkt",
-    "rhp_kkt_of", "rhp_fetch_solution", "rhp_fetch_iterate", "rhp_restart",
+    "rhp_kkt_of", "rhp_fetch_solution", "rhp_fetch_iterate", "rhp_restart", "rhp_any",
+    "rhp_partition_rows",
     "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_time_spmv", "rhp_profiler_range",
     "rhp_synchronize",
 ]
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",
-    "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_session_create",
+    "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_set_distributed",
+    "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
     "rhpdhg_session_layout", "rhpdhg_lp_read_mps", "rhpdhg_lp_view_of", "rhpdhg_lp_free",
@@ -240,6 +242,8 @@ def load_cuda() -> C.CDLL:
             "rhp_fetch_solution": [P, c_double_p, c_double_p, c_double_p],
             "rhp_fetch_iterate": [P, c_double_p, c_double_p, c_double_p, c_double_p],
             "rhp_restart": [P],
+            "rhp_any": [P, C.c_int, C.POINTER(C.c_int)],
+            "rhp_partition_rows": [C.POINTER(LpView), C.c_int, c_int64_p],
             "rhp_last_block_ms": [P, c_double_p],
             "rhp_timer": [P, C.c_int, c_double_p],
             "rhp_time_kernels": [P, C.c_int, c_double_p, c_double_p, c_double_p],
@@ -274,6 +278,7 @@ def load_host() -> C.CDLL:
         P = C.c_void_p
         sig = {
             "rhpdhg_set_device_options": [C.c_int, C.c_int, C.c_int64],
+            "rhpdhg_set_distributed": [C.c_int, C.c_int, C.c_void_p],
             "rhpdhg_session_create": [C.POINTER(LpView), C.POINTER(ConfigC), C.POINTER(P)],
             "rhpdhg_session_advance": [P, C.c_int64, C.POINTER(C.c_int32)],
             "rhpdhg_session_info": [P, c_int64_p, c_int64_p, C.POINTER(KktC), c_double_p,

@@ -19,13 +19,15 @@ namespace rhp {
 
 constexpr int kBlock = 256;          // threads per CTA for every hot kernel
 constexpr int kWarps = kBlock / 32;
-// 1024 nonzeros (4 per thread) x 4 resident CTAs per SM measured best on
-// B200 against 2048x2, 1024x3 and 512x6 (tools/spmv_probe.py)
+// 1024 nonzeros (4 per thread) x 3 resident CTAs per SM measured best for the
+// fused iteration kernels on B200 (C2: 5.18k iter/s vs 4.92k for 2048x2,
+// 4.82k for 2048x3, 4.62k for 1024x4 whose 224 KB of shared memory leaves
+// almost no L1; plain-SpMV probe in tools/spmv_probe.py)
 #ifndef RHP_TILE_NNZ
 #define RHP_TILE_NNZ 1024
 #endif
 #ifndef RHP_MIN_BLOCKS
-#define RHP_MIN_BLOCKS 4
+#define RHP_MIN_BLOCKS 3
 #endif
 constexpr int kMinBlocks = RHP_MIN_BLOCKS;  // resident CTAs per SM the SpMV is built for
 constexpr int kTileNnz = RHP_TILE_NNZ;      // nonzeros per stream tile
@@ -92,7 +94,8 @@ struct Ctl {
   // -- last-block tickets (one per finalizing kernel family)
   unsigned int ticket_dual, ticket_kkt, ticket_pow, ticket_spare;
   unsigned long long cond_handle;  // cudaGraphConditionalHandle of the block WHILE node
-  int32_t graph_mode, pad1;
+  int32_t graph_mode;
+  int32_t k1_token_pending;        // row-partitioned path: K1 ran, control not yet
   double* hist;                    // [block_limit] residual history of the current block
 };
 

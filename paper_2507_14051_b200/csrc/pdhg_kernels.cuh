@@ -94,6 +94,69 @@ struct EpiPrimal {
   }
 };
 
+// End-of-iteration control, one thread: fixed-point residual with its clamp
+// rules (pdhg.cpp:101-115), restart verdict (restart.cpp:54-69,
+// solver.cpp:162-169), k/total bookkeeping and the block-stop condition.
+// t1 = y-side sums {||dy||^2, dy.dax, ||y-y0||^2, ||y||^2, ||y_old||^2},
+// t3 = x-side sums {||dx||^2, ||x-x0||^2, ||x||^2, ||x_old||^2}.
+__device__ __forceinline__ void pdhg_control(Ctl* ctl, const double* t1, const double* t3,
+                                             int token) {
+  const double ps = ctl->primal_scale, ds = ctl->dual_scale;
+  // quadratic_form(dx, dy, d_ax) (pdhg.cpp:68-75)
+  const double diag = add(mul(ps, t3[0]), mul(ds, t1[0]));
+  const double q = add(diag, mul(2.0, t1[1]));
+  double r = 0.0;
+  int breakdown = 0;
+  if (q >= 0.0) {
+    r = sqrt(q);
+  } else if (q >= -1e-12 * smax(diag, 1e-300)) {
+    r = 0.0;
+  } else {
+    const double scale = add(mul(ps, t3[3]), mul(ds, t1[4]));
+    if (q >= -1e-24 * (1.0 + scale)) r = 0.0;
+    else breakdown = 1;
+  }
+  int64_t k = ctl->k, total = ctl->total;
+  int verdict = 0;
+  double r_anchor = ctl->r_anchor, r_prev = ctl->r_prev;
+  if (k == 0) {
+    r_anchor = r;
+    r_prev = r;
+  } else {
+    if (k >= 1 && isfinite(r_anchor)) {
+      if (r <= ctl->beta_s * r_anchor) verdict = 1;
+      else if (r <= ctl->beta_n * r_anchor && r > r_prev) verdict = 2;
+      else if (static_cast<double>(k) >= ctl->beta_a * static_cast<double>(total)) verdict = 3;
+    }
+    r_prev = r;
+  }
+  if (!ctl->restarts_enabled) verdict = 0;
+  k += 1;
+  total += 1;
+  const int64_t bi = ctl->block_iters;
+  if (ctl->record_history) ctl->hist[bi] = r;
+  const int check_due = (total % ctl->check_interval == 0) || verdict != 0;
+  const int stop =
+      check_due || breakdown || total >= ctl->iteration_limit || bi + 1 >= ctl->block_limit;
+  ctl->k = k;
+  ctl->total = total;
+  ctl->block_iters = bi + 1;
+  ctl->r_anchor = r_anchor;
+  ctl->r_prev = r_prev;
+  ctl->r_last = r;
+  ctl->q_last = q;
+  ctl->verdict = verdict;
+  ctl->check_due = check_due;
+  ctl->breakdown = breakdown;
+  ctl->stop = stop;
+  ctl->k1_token = token;
+  ctl->x_dist2 = t3[1];
+  ctl->x_norm2 = t3[2];
+  ctl->y_dist2 = t1[2];
+  ctl->y_norm2 = t1[3];
+  if (ctl->graph_mode) cudaGraphSetConditional(ctl->cond_handle, stop ? 0u : 1u);
+}
+
 // ------------------------------------------------------------------- K1 ----
 // inputs: y, ax, con_lb, con_ub, y0, ax0
 struct EpiDual {
@@ -110,6 +173,7 @@ struct EpiDual {
   int grid3;
   int n_multi3;            // multi-chunk rows of the A^T schedule and their
   const double* long_red3; //   primal partial slots
+  double* xchg;            // row-partitioned path: where the y-side sums go (else null)
   int token;               // launch index inside a plain (non-graph) block
   double sigma, sigma_inv, a, b, g, opg;
 
@@ -154,61 +218,67 @@ struct EpiDual {
     block_sum_partials<4>(part3, grid3, grid3, t3);
     add_slots<4>(long_red3, n_multi3, t3);
     if (threadIdx.x != 0) return;
-    const double ps = ctl->primal_scale, ds = ctl->dual_scale;
-    // quadratic_form(dx, dy, d_ax) (pdhg.cpp:68-75)
-    const double diag = add(mul(ps, t3[0]), mul(ds, t1[0]));
-    const double q = add(diag, mul(2.0, t1[1]));
-    double r = 0.0;
-    int breakdown = 0;
-    if (q >= 0.0) {
-      r = sqrt(q);
-    } else if (q >= -1e-12 * smax(diag, 1e-300)) {
-      r = 0.0;
-    } else {
-      const double scale = add(mul(ps, t3[3]), mul(ds, t1[4]));
-      if (q >= -1e-24 * (1.0 + scale)) r = 0.0;
-      else breakdown = 1;
+    if (xchg) {  // row-partitioned: publish the local y-side sums, control after the allreduce
+#pragma unroll
+      for (int q = 0; q < 5; ++q) xchg[q] = t1[q];
+      ctl->k1_token_pending = token;
+      return;
     }
-    int64_t k = ctl->k, total = ctl->total;
-    int verdict = 0;
-    double r_anchor = ctl->r_anchor, r_prev = ctl->r_prev;
-    if (k == 0) {
-      r_anchor = r;
-      r_prev = r;
-    } else {
-      if (k >= 1 && isfinite(r_anchor)) {
-        if (r <= ctl->beta_s * r_anchor) verdict = 1;
-        else if (r <= ctl->beta_n * r_anchor && r > r_prev) verdict = 2;
-        else if (static_cast<double>(k) >= ctl->beta_a * static_cast<double>(total)) verdict = 3;
-      }
-      r_prev = r;
-    }
-    if (!ctl->restarts_enabled) verdict = 0;
-    k += 1;
-    total += 1;
-    const int64_t bi = ctl->block_iters;
-    if (ctl->record_history) ctl->hist[bi] = r;
-    const int check_due = (total % ctl->check_interval == 0) || verdict != 0;
-    const int stop = check_due || breakdown || total >= ctl->iteration_limit ||
-                     bi + 1 >= ctl->block_limit;
-    ctl->k = k;
-    ctl->total = total;
-    ctl->block_iters = bi + 1;
-    ctl->r_anchor = r_anchor;
-    ctl->r_prev = r_prev;
-    ctl->r_last = r;
-    ctl->q_last = q;
-    ctl->verdict = verdict;
-    ctl->check_due = check_due;
-    ctl->breakdown = breakdown;
-    ctl->stop = stop;
-    ctl->k1_token = token;
-    ctl->x_dist2 = t3[1];
-    ctl->x_norm2 = t3[2];
-    ctl->y_dist2 = t1[2];
-    ctl->y_norm2 = t1[3];
-    if (ctl->graph_mode) cudaGraphSetConditional(ctl->cond_handle, stop ? 0u : 1u);
+    pdhg_control(ctl, t1, t3, token);
   }
+};
+
+// ------------------------------------------------- row-partitioned (NCCL) --
+// After the allreduce of [A_p^T y+_p partials (n) | y-side sums (5)]:
+// one CTA reduces the (replicated, rank-identical) x-side partials and runs
+// the control on the global sums.
+__global__ void __launch_bounds__(kBlock) k_dist_control(Ctl* ctl, const double* part3, int grid3,
+                                                         int n_multi3, const double* long_red3,
+                                                         const double* xsums, int token) {
+  if (!ctl->graph_mode && ctl->k1_token_pending != token && !ctl->bench) return;
+  double t3[4];
+  block_sum_partials<4>(part3, grid3, grid3, t3);
+  add_slots<4>(long_red3, n_multi3, t3);
+  if (threadIdx.x == 0) {
+    double t1[5];
+    for (int q = 0; q < 5; ++q) t1[q] = __ldcg(xsums + q);
+    pdhg_control(ctl, t1, t3, token);
+  }
+}
+
+// K2c: aty Halpern update + next primal step from the allreduced A^T y+.
+// inputs: aty+ (allreduced), aty, aty0, x, c, var_lb, var_ub, x0
+struct EpiAtyDist {
+  static constexpr int NRED = 4;
+  static constexpr int NIN = 8;
+  Ctl* ctl;
+  double* aty;
+  PrimalOut o;
+  const double* in[NIN];
+  int token;
+  double a, b, a2, b2, g, opg, tau;
+  int stop;
+  __device__ bool enter() {
+    if (!ctl->graph_mode && ctl->k1_token != token && !ctl->bench) return false;
+    const int64_t k = ctl->k;
+    a = halpern_a(k - 1);
+    b = halpern_b(k - 1);
+    a2 = halpern_a(k);
+    b2 = halpern_b(k);
+    g = ctl->gamma;
+    opg = 1.0 + g;
+    tau = ctl->tau;
+    stop = ctl->stop && !ctl->bench;
+    return true;
+  }
+  __device__ void row(int64_t j, double, const double* e, int st, double (&acc)[NRED]) {
+    const double atyn = affine(a, opg, g, b, e[0], e[st], e[2 * st]);
+    aty[j] = atyn;
+    if (!stop)
+      primal_col(o, j, atyn, e[3 * st], e[4 * st], e[5 * st], e[6 * st], e[7 * st], tau, a2, opg,
+                 g, b2, acc);
+  }
+  __device__ void walk_done() {}
 };
 
 // ------------------------------------------------------------------- K2 ----
@@ -258,7 +328,11 @@ struct EpiStore {
   static constexpr bool FINAL = false;
   double* out;
   const double* in[1];
-  __device__ bool enter() { return true; }
+  Ctl* ctl;   // optional guard (row-partitioned A^T pass): run only after K1 of `token`
+  int token;
+  __device__ bool enter() {
+    return !ctl || ctl->graph_mode || ctl->bench || ctl->k1_token_pending == token;
+  }
   __device__ void row(int64_t i, double s, const double*, int, double (&)[NRED]) { out[i] = s; }
   __device__ void finalize(const Sched&, const double*, int) {}
 };
@@ -400,5 +474,83 @@ struct EpiKktCol {
     }
   }
 };
+
+// ---------------------------------------- row-partitioned KKT and power ----
+// KA (local rows): as EpiKktRow, the last block publishes the 4 row-side sums
+// into the exchange buffer that is allreduced with the A^T partial.
+struct EpiKktRowDist : EpiKktRow {
+  static constexpr bool FINAL = true;
+  double* xsums;  // 4 doubles
+  __device__ void finalize(const Sched& s, const double* part, int grid) {
+    double t[4];
+    block_sum_partials<4>(part, grid, grid, t);
+    add_long_slots<4>(s, t);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < 4; ++q) xsums[q] = t[q];
+  }
+};
+
+// KB (all columns, redundant on every rank): as EpiKktCol with the allreduced
+// A^T y as input 0. inputs: aty (allreduced), x, D_col, c, var_lb, var_ub
+struct EpiKktColDist {
+  static constexpr int NRED = 6;
+  static constexpr int NIN = 6;
+  EpiKktCol col;  // row() logic; col.in[] = in[1..5]
+  const double* in[NIN];
+  __device__ bool enter() { return true; }
+  __device__ void row(int64_t j, double, const double* e, int st, double (&acc)[NRED]) {
+    col.row(j, e[0], e + st, st, acc);
+  }
+  __device__ void walk_done() {}
+};
+
+__global__ void __launch_bounds__(kBlock) k_kkt_dist_finalize(Ctl* ctl, const double* part,
+                                                              int grid, int n_multi,
+                                                              const double* long_red,
+                                                              const double* xsums) {
+  double tc[6];
+  block_sum_partials<6>(part, grid, grid, tc);
+  add_slots<6>(long_red, n_multi, tc);
+  if (threadIdx.x == 0) {
+    ctl->kkt_nan_y = __ldcg(xsums + 0);
+    ctl->kkt_viol2 = __ldcg(xsums + 1);
+    ctl->kkt_py_inf = __ldcg(xsums + 2);
+    ctl->kkt_py = __ldcg(xsums + 3);
+    ctl->kkt_nan_x = tc[0];
+    ctl->kkt_pr_inf = tc[1];
+    ctl->kkt_pr = tc[2];
+    ctl->kkt_eq2 = tc[3];
+    ctl->kkt_cone2 = tc[4];
+    ctl->kkt_cx = tc[5];
+  }
+}
+
+// power iteration, w = allreduced A^T (A_p v): inputs w, v
+struct EpiPowerDist {
+  static constexpr int NRED = 2;
+  static constexpr int NIN = 2;
+  double* w;
+  const double* in[NIN];
+  __device__ bool enter() { return true; }
+  __device__ void row(int64_t j, double, const double* e, int st, double (&acc)[NRED]) {
+    const double s = e[0];
+    w[j] = s;
+    acc[0] = fma(e[st], s, acc[0]);
+    acc[1] = fma(s, s, acc[1]);
+  }
+  __device__ void walk_done() {}
+};
+
+__global__ void __launch_bounds__(kBlock) k_power_dist_finalize(Ctl* ctl, const double* part,
+                                                                int grid, int n_multi,
+                                                                const double* long_red) {
+  double t[2];
+  block_sum_partials<2>(part, grid, grid, t);
+  add_slots<2>(long_red, n_multi, t);
+  if (threadIdx.x == 0) {
+    ctl->pw_vw = t[0];
+    ctl->pw_ww = t[1];
+  }
+}
 
 }  // namespace rhp

@@ -130,6 +130,18 @@ struct rhp_ctx {
   int64_t host_total = 0;  // mirror of ctl->total after the last block
   int64_t host_check_interval = 64, host_iteration_limit = INT64_MAX;
   std::vector<double> hbuf;  // host scratch
+  // row-partitioned multi-GPU
+  bool dist = false;
+  int rank = 0, world = 1;
+  std::vector<int64_t> offsets;  // world+1 row offsets of the partition
+  int64_t max_local = 0;         // largest local row count
+  double* xchg = nullptr;        // [n + 16]: A_p^T partial | scalar sums (allreduced)
+  double* ypad = nullptr;        // [max_local]
+  double* ygather = nullptr;     // [world * max_local]
+  int64_t* agree = nullptr;      // 1 int64 for host-decision agreement
+#ifdef RHP_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
 };
 
 namespace {
@@ -290,9 +302,54 @@ EpiAty epi_aty(rhp_ctx& c, int token) {
   return e;
 }
 
+void allreduce(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
+#ifdef RHP_WITH_NCCL
+  if (ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c.comm, s) != ncclSuccess)
+    throw CudaError("ncclAllReduce failed");
+#else
+  (void)c, (void)buf, (void)count, (void)s;
+  throw CudaError("built without NCCL");
+#endif
+}
+
+void allreduce_max(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
+#ifdef RHP_WITH_NCCL
+  if (ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, c.comm, s) != ncclSuccess)
+    throw CudaError("ncclAllReduce(max) failed");
+#else
+  (void)c, (void)buf, (void)count, (void)s;
+  throw CudaError("built without NCCL");
+#endif
+}
+
 void launch_iteration(rhp_ctx& c, int token, cudaStream_t s) {
-  launch_spmv(c, c.A, c.grid_a, c.xp, epi_dual(c, token), c.part1, &c.ctl->ticket_dual, s);
-  launch_spmv(c, c.At, c.grid_at, c.yp, epi_aty(c, token), c.part3, nullptr, s);
+  if (!c.dist) {
+    launch_spmv(c, c.A, c.grid_a, c.xp, epi_dual(c, token), c.part1, &c.ctl->ticket_dual, s);
+    launch_spmv(c, c.At, c.grid_at, c.yp, epi_aty(c, token), c.part3, nullptr, s);
+    return;
+  }
+  // row-partitioned: local A x+ with the dual epilogue (y-side sums -> xchg[n..]),
+  // local A_p^T y+_p -> xchg[0..n), one allreduce, control, aty/primal epilogue
+  EpiDual d = epi_dual(c, token);
+  d.xchg = c.xchg + c.n;
+  launch_spmv(c, c.A, c.grid_a, c.xp, d, c.part1, &c.ctl->ticket_dual, s);
+  EpiStore st = store_into(c.xchg);
+  st.ctl = c.ctl;
+  st.token = token;
+  launch_spmv(c, c.At, c.grid_at, c.yp, st, nullptr, nullptr, s);
+  allreduce(c, c.xchg, static_cast<size_t>(c.n) + 5, s);
+  k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, c.grid_at, c.At.sched.n_multi,
+                                      c.At.long_red, c.xchg + c.n, token);
+  CK(cudaGetLastError());
+  EpiAtyDist e{};
+  e.ctl = c.ctl;
+  e.aty = c.aty;
+  e.o = primal_out(c);
+  const double* in[] = {c.xchg, c.aty, c.aty0, c.x, c.c, c.vl, c.vu, c.x0};
+  for (int k = 0; k < EpiAtyDist::NIN; ++k) e.in[k] = in[k];
+  e.token = token;
+  epilogue_walk<EpiAtyDist><<<c.grid_at, kBlock, 0, s>>>(c.At.sched, e, c.part3);
+  CK(cudaGetLastError());
 }
 
 void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
@@ -367,7 +424,7 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
   er.in[1] = c.rs;
   er.in[2] = c.clo;
   er.in[3] = c.cuo;
-  launch_spmv(c, c.A, c.grid_a, xs, er, c.partA, nullptr, c.stream);
+  if (!c.dist) launch_spmv(c, c.A, c.grid_a, xs, er, c.partA, nullptr, c.stream);
   EpiKktCol ec{};
   ec.ctl = c.ctl;
   ec.aty_refresh = refresh ? c.aty : nullptr;
@@ -382,7 +439,27 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
   ec.grid_row = c.grid_a;
   ec.n_multi_row = c.A.sched.n_multi;
   ec.long_red_row = c.A.long_red;
-  launch_spmv(c, c.At, c.grid_at, ys, ec, c.partAt, &c.ctl->ticket_kkt, c.stream);
+  if (!c.dist) {
+    launch_spmv(c, c.At, c.grid_at, ys, ec, c.partAt, &c.ctl->ticket_kkt, c.stream);
+  } else {
+    // local rows; the last block publishes the row-side sums into xchg[n+8..n+12)
+    EpiKktRowDist rd{};
+    static_cast<EpiKktRow&>(rd) = er;
+    rd.xsums = c.xchg + c.n + 8;
+    launch_spmv(c, c.A, c.grid_a, xs, rd, c.partA, &c.ctl->ticket_kkt, c.stream);
+    launch_spmv(c, c.At, c.grid_at, ys, store_into(c.xchg), nullptr, nullptr, c.stream);
+    allreduce(c, c.xchg, static_cast<size_t>(c.n) + 16, c.stream);
+    EpiKktColDist cd{};
+    cd.col = ec;
+    const double* in[] = {c.xchg, xs, c.cs, c.co, c.vlo, c.vuo};
+    for (int k = 0; k < EpiKktColDist::NIN; ++k) cd.in[k] = in[k];
+    epilogue_walk<EpiKktColDist><<<c.grid_at, kBlock, 0, c.stream>>>(c.At.sched, cd, c.partAt);
+    CK(cudaGetLastError());
+    k_kkt_dist_finalize<<<1, kBlock, 0, c.stream>>>(c.ctl, c.partAt, c.grid_at,
+                                                    c.At.sched.n_multi, c.At.long_red,
+                                                    c.xchg + c.n + 8);
+    CK(cudaGetLastError());
+  }
   pull_ctl(c);
   const Ctl& h = *c.ctl_host;
   out->primal_value = h.kkt_cx;
@@ -462,8 +539,15 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     opt.block_limit = 64;
     if (opt_in) opt = *opt_in;
     if (opt.block_limit < 1) opt.block_limit = 64;
-    if (opt.world_size != 1)
-      throw std::invalid_argument("rhp_create: multi-GPU contexts go through rhp_create_dist");
+    if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size)
+      throw std::invalid_argument("rhp_create: bad rank/world_size");
+    if (opt.world_size > 1 && !opt.nccl_id)
+      throw std::invalid_argument("rhp_create: world_size > 1 needs an NCCL unique id");
+    // row-partitioned path (also with one rank when an id is given: parity tests)
+    c->dist = opt.nccl_id != nullptr;
+    c->rank = opt.rank;
+    c->world = opt.world_size;
+    if (c->dist) opt.use_graph = 0;  // NCCL calls are launched from the host loop
     c->opt = opt;
     if (lp->num_cons < 0 || lp->num_vars < 0 || lp->nnz < 0)
       throw std::invalid_argument("matrix dimensions must be nonnegative");
@@ -479,7 +563,14 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->tev0));
     CK(cudaEventCreate(&c->tev1));
-    build_layout(*lp, 0, lp->num_cons, c->L);
+    if (c->dist) {
+      c->offsets = partition_rows(*lp, c->world);
+      for (int r = 0; r < c->world; ++r)
+        c->max_local = std::max(c->max_local, c->offsets[r + 1] - c->offsets[r]);
+      build_layout(*lp, c->offsets[c->rank], c->offsets[c->rank + 1], c->L);
+    } else {
+      build_layout(*lp, 0, lp->num_cons, c->L);
+    }
     const HostLayout& L = c->L;
     c->m = L.m;
     c->n = L.n;
@@ -511,7 +602,8 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     // grids: persistent, a multiple of the SM count, never more than tiles
     // one grid per operator: every kernel walking it must see the same CTA count
     const int occ_store = prepare_spmv<EpiStore>();
-    const int occ_a = std::min({prepare_spmv<EpiDual>(), prepare_spmv<EpiKktRow>(), occ_store});
+    const int occ_a = std::min({prepare_spmv<EpiDual>(), prepare_spmv<EpiKktRow>(),
+                                prepare_spmv<EpiKktRowDist>(), occ_store});
     const int occ_at = std::min({prepare_spmv<EpiAty>(), prepare_spmv<EpiKktCol>(),
                                  prepare_spmv<EpiPowerW>(), occ_store});
     auto clampg = [](int64_t tiles, int64_t cap) {
@@ -540,7 +632,21 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       CK(cudaMemsetAsync(p2, 0, std::max<size_t>(n, 1) * sizeof(double), s));
     for (double* p2 : {c->y, c->ax, c->y0, c->ax0, c->yp, c->yout, c->pav})
       CK(cudaMemsetAsync(p2, 0, std::max<size_t>(m, 1) * sizeof(double), s));
+    c->xchg = dev_alloc<double>(n + 16);
     CK(cudaStreamSynchronize(s));
+    if (c->dist) {
+      c->ypad = dev_alloc<double>(static_cast<size_t>(c->max_local));
+      c->ygather = dev_alloc<double>(static_cast<size_t>(c->max_local) * c->world);
+      c->agree = dev_alloc<int64_t>(1);
+#ifdef RHP_WITH_NCCL
+      ncclUniqueId id;
+      std::memcpy(&id, opt.nccl_id, sizeof(id));
+      if (ncclCommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess)
+        throw CudaError("ncclCommInitRank failed");
+#else
+      throw CudaError("built without NCCL");
+#endif
+    }
   });
   if (rc != RHPDHG_OK) {
     rhp_destroy(c);
@@ -560,8 +666,12 @@ int rhp_destroy(rhp_ctx* c) {
   for (double* p : {c->c, c->vl, c->vu, c->cl, c->cu, c->co, c->vlo, c->vuo, c->clo, c->cuo,
                     c->rs, c->cs, c->x, c->y, c->ax, c->aty, c->x0, c->y0, c->ax0, c->aty0,
                     c->xp, c->yp, c->xout, c->yout, c->rcout, c->pv, c->pw, c->pav, c->part1,
-                    c->part3, c->partA, c->partAt, c->hist})
+                    c->part3, c->partA, c->partAt, c->hist, c->xchg, c->ypad, c->ygather})
     if (p) cudaFree(p);
+  if (c->agree) cudaFree(c->agree);
+#ifdef RHP_WITH_NCCL
+  if (c->comm) ncclCommDestroy(c->comm);
+#endif
   if (c->ctl) cudaFree(c->ctl);
   if (c->ctl_host) cudaFreeHost(c->ctl_host);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -605,7 +715,13 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
       double* wT = c->At.v;
       for (int pass = 0; pass < ruiz_iterations; ++pass) {
         k_row_absmax_sqrt<<<gr, kBlock, 0, s>>>(c->A.rp, wA, m, rmax);
-        k_row_absmax_sqrt<<<gr, kBlock, 0, s>>>(c->At.rp, wT, n, cmax);
+        if (!c->dist) {
+          k_row_absmax_sqrt<<<gr, kBlock, 0, s>>>(c->At.rp, wT, n, cmax);
+        } else {  // column maxima over all ranks' rows (max is exact: order-free)
+          k_row_absmax_raw<<<gr, kBlock, 0, s>>>(c->At.rp, wT, n, cmax);
+          allreduce_max(*c, cmax, static_cast<size_t>(n), s);
+          k_sqrt_or_one<<<gr, kBlock, 0, s>>>(cmax, n);
+        }
         k_ruiz_divide<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.ci, wA, m, rmax, cmax);
         k_ruiz_divide<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, wT, n, cmax, rmax);
         k_vec_div<<<gr, kBlock, 0, s>>>(c->rs, rmax, m);
@@ -621,7 +737,14 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
         double* rn = c->pav;
         double* cn = c->pw;
         k_pc_rows<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.v, m, rn);
-        k_pc_cols<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v_orig, n, c->rs, c->cs, cn);
+        if (!c->dist) {
+          k_pc_cols<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v_orig, n, c->rs, c->cs, cn);
+        } else {  // per-rank partial 1-norms, summed across ranks
+          k_pc_cols_raw<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v_orig, n, c->rs, c->cs,
+                                              cn);
+          allreduce(*c, cn, static_cast<size_t>(n), s);
+          k_inv_sqrt_or_one<<<gr, kBlock, 0, s>>>(cn, n);
+        }
         // apply_scales(ruiz-scaled, rn, cn) in place
         k_scale_values<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.ci, c->A.v, c->A.v, m, rn, cn);
         k_scale_values<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v, c->At.v, n, cn, rn);
@@ -674,11 +797,25 @@ int rhp_power_begin(rhp_ctx* c, const double* v0) {
 int rhp_power_step(rhp_ctx* c, double* vw, double* ww) {
   return guarded([&] {
     launch_spmv(*c, c->A, c->grid_a, c->pv, store_into(c->pav), nullptr, nullptr, c->stream);
-    EpiPowerW e{};
-    e.ctl = c->ctl;
-    e.w = c->pw;
-    e.in[0] = c->pv;
-    launch_spmv(*c, c->At, c->grid_at, c->pav, e, c->partAt, &c->ctl->ticket_pow, c->stream);
+    if (!c->dist) {
+      EpiPowerW e{};
+      e.ctl = c->ctl;
+      e.w = c->pw;
+      e.in[0] = c->pv;
+      launch_spmv(*c, c->At, c->grid_at, c->pav, e, c->partAt, &c->ctl->ticket_pow, c->stream);
+    } else {  // w = sum over ranks of A_p^T (A_p v), then v.w and w.w redundantly
+      launch_spmv(*c, c->At, c->grid_at, c->pav, store_into(c->xchg), nullptr, nullptr,
+                  c->stream);
+      allreduce(*c, c->xchg, static_cast<size_t>(c->n), c->stream);
+      EpiPowerDist e{};
+      e.w = c->pw;
+      e.in[0] = c->xchg;
+      e.in[1] = c->pv;
+      epilogue_walk<EpiPowerDist><<<c->grid_at, kBlock, 0, c->stream>>>(c->At.sched, e, c->partAt);
+      k_power_dist_finalize<<<1, kBlock, 0, c->stream>>>(c->ctl, c->partAt, c->grid_at,
+                                                         c->At.sched.n_multi, c->At.long_red);
+      CK(cudaGetLastError());
+    }
     pull_ctl(*c);
     *vw = c->ctl_host->pw_vw;
     *ww = c->ctl_host->pw_ww;
@@ -834,11 +971,65 @@ int rhp_kkt_of(rhp_ctx* c, const double* x, const double* y, rhp_kkt_sums* out) 
   });
 }
 
+// Row-partitioned: every rank receives the full m-vector (rank blocks are
+// contiguous original rows; NCCL allgather of the padded local blocks).
+void gather_rows(rhp_ctx& c, const double* dev_local, double* host_full) {
+#ifdef RHP_WITH_NCCL
+  cudaStream_t s = c.stream;
+  const size_t ml = static_cast<size_t>(c.m), mx = static_cast<size_t>(c.max_local);
+  CK(cudaMemsetAsync(c.ypad, 0, std::max<size_t>(mx, 1) * sizeof(double), s));
+  if (ml) CK(cudaMemcpyAsync(c.ypad, dev_local, ml * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (ncclAllGather(c.ypad, c.ygather, mx, ncclDouble, c.comm, s) != ncclSuccess)
+    throw CudaError("ncclAllGather failed");
+  std::vector<double> all(mx * static_cast<size_t>(c.world));
+  if (!all.empty())
+    CK(cudaMemcpyAsync(all.data(), c.ygather, all.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       s));
+  CK(cudaStreamSynchronize(s));
+  for (int r = 0; r < c.world; ++r)
+    std::copy(all.begin() + static_cast<ptrdiff_t>(r * mx),
+              all.begin() + static_cast<ptrdiff_t>(r * mx + (c.offsets[r + 1] - c.offsets[r])),
+              host_full + c.offsets[r]);
+#else
+  (void)c, (void)dev_local, (void)host_full;
+  throw CudaError("built without NCCL");
+#endif
+}
+
 int rhp_fetch_solution(rhp_ctx* c, double* x, double* y, double* rcost) {
   return guarded([&] {
     if (x) download_perm(x, c->xout, c->L.pcol, c->hbuf, c->stream);
-    if (y) download_perm(y, c->yout, local_rows(*c), c->hbuf, c->stream);
+    if (y) {
+      if (c->dist) gather_rows(*c, c->yout, y);
+      else download_perm(y, c->yout, local_rows(*c), c->hbuf, c->stream);
+    }
     if (rcost) download_perm(rcost, c->rcout, c->L.pcol, c->hbuf, c->stream);
+  });
+}
+
+int rhp_partition_rows(const rhpdhg_lp_view* lp, int world_size, int64_t* offsets) {
+  return guarded([&] {
+    if (world_size < 1) throw std::invalid_argument("world_size must be >= 1");
+    const std::vector<int64_t> off = partition_rows(*lp, world_size);
+    std::copy(off.begin(), off.end(), offsets);
+  });
+}
+
+int rhp_any(rhp_ctx* c, int flag, int* any) {
+  return guarded([&] {
+    if (!c->dist) {
+      *any = flag;
+      return;
+    }
+#ifdef RHP_WITH_NCCL
+    int64_t v = flag ? 1 : 0;
+    CK(cudaMemcpyAsync(c->agree, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
+    if (ncclAllReduce(c->agree, c->agree, 1, ncclInt64, ncclMax, c->comm, c->stream) != ncclSuccess)
+      throw CudaError("ncclAllReduce(agree) failed");
+    CK(cudaMemcpyAsync(&v, c->agree, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *any = v != 0;
+#endif
   });
 }
 

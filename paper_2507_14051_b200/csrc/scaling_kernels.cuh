@@ -105,6 +105,44 @@ __global__ void k_apply_row_scales(double* lb, double* ub, const double* rs, int
   }
 }
 
+// Row-partitioned scaling: per-rank raw column maxima / 1-norm partials are
+// combined with an NCCL allreduce (max / sum) before the sqrt step.
+__global__ void k_row_absmax_raw(const int64_t* rp, const double* w, int64_t rows, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * kBlock) {
+    double mx = 0.0;
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const double a = fabs(w[e]);
+      if (a > mx) mx = a;
+    }
+    out[i] = mx;
+  }
+}
+
+__global__ void k_sqrt_or_one(double* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kBlock)
+    v[i] = v[i] > 0.0 ? sqrt(v[i]) : 1.0;
+}
+
+__global__ void k_pc_cols_raw(const int64_t* rp, const int32_t* ci, const double* a_orig,
+                              int64_t rows, const double* rs, const double* cs, double* out) {
+  for (int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x; j < rows;
+       j += (int64_t)gridDim.x * kBlock) {
+    const double cj = cs[j];
+    double acc = 0.0;
+    for (int64_t e = rp[j]; e < rp[j + 1]; ++e)
+      acc = add(acc, fabs(mul(mul(rs[ci[e]], a_orig[e]), cj)));
+    out[j] = acc;
+  }
+}
+
+__global__ void k_inv_sqrt_or_one(double* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kBlock)
+    v[i] = v[i] > 0.0 ? __ddiv_rn(1.0, sqrt(v[i])) : 1.0;
+}
+
 // v = w / ||w|| (pdhg.cpp:149)
 __global__ void k_normalize(double* v, const double* w, double wn, int64_t n) {
   for (int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x; j < n;

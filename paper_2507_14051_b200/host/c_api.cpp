@@ -180,6 +180,22 @@ int rhpdhg_set_device_options(int device, int use_graph, int64_t block_limit) {
   });
 }
 
+int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id) {
+  return guarded([&] {
+    if (world_size < 1 || rank < 0 || rank >= world_size) throw UsageError("bad rank/world_size");
+    if (world_size > 1 && !nccl_id) throw UsageError("world_size > 1 needs an NCCL unique id");
+    DeviceOptions& d = default_device_options();
+    d.rank = rank;
+    d.world_size = world_size;
+    if (nccl_id) {
+      const char* p = static_cast<const char*>(nccl_id);
+      d.nccl_id.assign(p, p + 128);
+    } else {
+      d.nccl_id.clear();
+    }
+  });
+}
+
 int rhpdhg_solve_csr(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg, rhpdhg_report_c* out,
                      double* x, double* y, double* rc, double* hist, int64_t hist_cap) {
   return guarded([&] {

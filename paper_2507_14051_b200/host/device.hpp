@@ -67,4 +67,20 @@ inline rhp_options options(int device, bool use_graph, long block_limit) {
   return o;
 }
 
+// Full options of a solve, including the row-partitioned multi-GPU fields
+// (the id buffer must outlive rhp_create).
+template <class DeviceOptionsT>
+inline rhp_options options(const DeviceOptionsT& d) {
+  rhp_options o = options(d.device, d.use_graph, d.block_limit);
+  o.rank = d.rank;
+  o.world_size = d.world_size;
+  if (!d.nccl_id.empty()) {
+    if (d.nccl_id.size() != 128) throw UsageError("nccl_id must be 128 bytes");
+    o.nccl_id = d.nccl_id.data();
+  } else if (d.world_size > 1) {
+    throw UsageError("world_size > 1 needs the NCCL unique id of rank 0");
+  }
+  return o;
+}
+
 }  // namespace rhpdhg::detail

@@ -124,8 +124,7 @@ Session::Session(const LpProblem& problem, const SolverConfig& cfg, const Device
   problem.validate();
   t0_ = Clock::now();
   const Index n = problem.num_vars();
-  dev_ = std::make_unique<detail::Device>(
-      detail::view_of(problem), detail::options(dopt.device, dopt.use_graph, dopt.block_limit));
+  dev_ = std::make_unique<detail::Device>(detail::view_of(problem), detail::options(dopt));
   rhp_ctx* c = dev_->get();
   // (1) diagonal preconditioning on the device (solver.cpp:72-78)
   detail::ok(rhp_scale(c, cfg.scaling_enabled ? 1 : 0, cfg.ruiz_iterations, cfg.pock_chambolle ? 1 : 0),
@@ -191,7 +190,9 @@ bool Session::step() {
     decided_ = true;
     return false;
   }
-  if (since(t0_) >= cfg_.time_limit_seconds) {
+  int out_of_time = since(t0_) >= cfg_.time_limit_seconds ? 1 : 0;
+  detail::ok(rhp_any(c, out_of_time, &out_of_time), "rhp_any");  // same verdict on every rank
+  if (out_of_time) {
     status_ = SolveStatus::time_limit;
     decided_ = true;
     return false;

@@ -372,6 +372,34 @@ def set_device_options(device: int = 0, use_graph: bool = True, block_limit: int
                  lib.rhpdhg_last_error().decode())
 
 
+def nccl_unique_id() -> bytes:
+    """rank 0: a fresh 128-byte ncclUniqueId to share with the other ranks."""
+    lib = capi.load_cuda()
+    buf = C.create_string_buffer(128)
+    raise_status(lib.rhp_nccl_unique_id(buf), lib.rhp_last_error().decode(errors="replace"))
+    return buf.raw
+
+
+def set_distributed(rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None) -> None:
+    """Row-partitioned multi-GPU solves: this process is `rank` of
+    `world_size`; every rank solves the FULL problem with the same config."""
+    lib = capi.load_host()
+    idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    raise_status(lib.rhpdhg_set_distributed(rank, world_size, idbuf),
+                 lib.rhpdhg_last_error().decode(errors="replace"))
+
+
+def partition_rows(lp: LpProblem, world_size: int) -> np.ndarray:
+    """The row partition the multi-GPU path uses (GPU-free host logic)."""
+    lib = capi.load_cuda()
+    out = np.zeros(world_size + 1, dtype=np.int64)
+    view = lp.view()
+    raise_status(lib.rhp_partition_rows(C.byref(view), world_size,
+                                        out.ctypes.data_as(capi.c_int64_p)),
+                 lib.rhp_last_error().decode(errors="replace"))
+    return out
+
+
 class Session:
     """Resumable solve (rhpdhg_session_*): setup in the constructor, then
     advance() in slices of PDHG iterations, then finish() -> SolutionReport."""

@@ -1,0 +1,141 @@
+"""Row-partitioned multi-GPU path.
+
+CPU (gloo, world_size 2): the partition the device path uses
+(rhp_partition_rows, host code) covers the rows exactly once with balanced
+nonzeros, and the exchange algebra of one PDHG iteration — local A_p x, the
+allreduce of the A_p^T y_p partials plus the y-side sums, the column-max and
+1-norm allreduces of the scaling — reproduces the single-process quantities
+(oracle arithmetic on each rank's row block).
+
+GPU (-m gpu): the partitioned device path (K1d / A_p^T / NCCL allreduce /
+control / K2c, distributed scaling, power iteration and KKT) run with one
+NCCL rank is bit-identical to the single-GPU path.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import support
+from paper_2507_14051_b200 import LpProblem, SolverConfig, solve
+from paper_2507_14051_b200.generators import c1_small, random_rows_lp
+from paper_2507_14051_b200.lp import nccl_unique_id, partition_rows, set_distributed
+
+
+def block(lp: LpProblem, r0: int, r1: int) -> LpProblem:
+    """Rows [r0, r1) of lp as their own LP (the rank-local operator)."""
+    b, e = lp.row_ptr[r0], lp.row_ptr[r1]
+    return LpProblem(r1 - r0, lp.num_vars, lp.row_ptr[r0:r1 + 1] - b, lp.col_index[b:e],
+                     lp.values[b:e], lp.objective, lp.var_lb, lp.var_ub, lp.con_lb[r0:r1],
+                     lp.con_ub[r0:r1])
+
+
+def ragged():
+    L = np.random.default_rng(5).integers(0, 60, 700)
+    L[::97] = 3000  # long rows
+    return random_rows_lp(17, 700, 900, L)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_partition_covers_rows_and_balances_nnz(world):
+    lp = ragged()
+    off = partition_rows(lp, world)
+    assert off[0] == 0 and off[-1] == lp.num_cons and np.all(np.diff(off) >= 0)
+    w = np.diff(lp.row_ptr) + 1
+    per = [w[off[r]:off[r + 1]].sum() for r in range(world)]
+    assert max(per) <= w.sum() / world + w.max() + 1
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        O = support.oracle()
+        lp = ragged()
+        off = partition_rows(lp, world)
+        loc = block(lp, int(off[rank]), int(off[rank + 1]))
+        rng = np.random.default_rng(0)
+        x = rng.uniform(-1, 1, lp.num_vars)  # replicated
+        y = rng.uniform(-1, 1, lp.num_cons)
+        y_loc = y[off[rank]:off[rank + 1]]
+        # A x is local; A^T y = sum of the ranks' partials (one allreduce)
+        ax_loc = support.spmv_with(O, loc, x)
+        xchg = torch.from_numpy(np.concatenate([support.spmv_with(O, loc, y_loc, True),
+                                                [float(np.dot(y_loc, y_loc))]]))
+        dist.all_reduce(xchg)
+        # scaling: column maxima (max-allreduce) and column 1-norms (sum)
+        cmax = torch.zeros(lp.num_vars, dtype=torch.float64)
+        cnorm = torch.zeros(lp.num_vars, dtype=torch.float64)
+        for i in range(loc.num_cons):
+            s, e = loc.row_ptr[i], loc.row_ptr[i + 1]
+            cols, vals = loc.col_index[s:e], np.abs(loc.values[s:e])
+            cmax[cols] = torch.maximum(cmax[cols], torch.from_numpy(vals))
+            cnorm[cols] += torch.from_numpy(vals)
+        dist.all_reduce(cmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnorm)
+        q.put((rank, int(off[rank]), ax_loc, xchg.numpy(), cmax.numpy(), cnorm.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_partition_exchange_matches_single_process_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    lp = ragged()
+    O = support.oracle()
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, lp.num_vars)
+    y = rng.uniform(-1, 1, lp.num_cons)
+    ax = np.concatenate([r[2] for r in res])
+    assert np.array_equal(ax, support.spmv_with(O, lp, x))  # local rows: same sums
+    aty = support.spmv_with(O, lp, y, True)
+    for _, _, _, xchg, cmax, cnorm in res:
+        assert np.array_equal(xchg, res[0][3])  # identical on every rank
+        assert np.allclose(xchg[:-1], aty, rtol=1e-13, atol=1e-13)
+        assert xchg[-1] == pytest.approx(float(np.dot(y, y)), rel=1e-14)
+        A = lp.to_dense()
+        assert np.array_equal(cmax, np.abs(A).max(axis=0))  # exact
+        assert np.allclose(cnorm, np.abs(A).sum(axis=0), rtol=1e-14)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("maker", [lambda: c1_small(m=400, n=700), ragged,
+                                   lambda: support.lp_from_json(
+                                       support.load_golden("random_feasible.json")
+                                       ["instances"][-1]["lp"])],
+                         ids=["c1_small", "ragged_long_rows", "rfl_5002"])
+def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker):
+    lp = maker()
+    cfg = SolverConfig(epsilon=1e-7, record_residual_history=True)
+    single = solve(lp, cfg)
+    try:
+        set_distributed(0, 1, nccl_unique_id())
+        part = solve(lp, cfg)
+    finally:
+        set_distributed(0, 1, None)
+    assert part.status == single.status
+    assert part.iterations == single.iterations and part.restart_count == single.restart_count
+    assert part.objective == single.objective
+    assert np.array_equal(part.x, single.x) and np.array_equal(part.y, single.y)
+    assert np.array_equal(part.fixed_point_residual_history, single.fixed_point_residual_history)
+    assert part.matrix_norm_estimate == single.matrix_norm_estimate

@@ -18,6 +18,7 @@ struct DeviceOptions {
   int device = 0;
   bool use_graph = true;   // CUDA graph with a conditional WHILE node per block
   long block_limit = 64;   // PDHG iterations per device block at most
+  int resident = -1;       // small LPs: one cluster runs whole blocks (-1 auto, 0 off, 1 on)
   // Row-partitioned multi-GPU solve (one process per GPU): every rank calls
   // solve() on the FULL problem with the same config; rank 0's 128-byte
   // ncclUniqueId (rhp_nccl_unique_id) is shared out of band. An id with

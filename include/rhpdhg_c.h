@@ -168,6 +168,8 @@ int rhpdhg_set_device_options(int device, int use_graph, int64_t block_limit);
  * 128-byte NCCL unique id (rhp_nccl_unique_id in rhpdhg_cuda.h). nccl_id NULL
  * with world_size 1 restores single-GPU solves. */
 int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id);
+/* Small-LP cluster-resident device blocks: -1 auto (default), 0 off, 1 on. */
+int rhpdhg_set_resident(int mode);
 
 /* Resumable solve (extension used by benchmarks and long-running callers):
  * create = validation + upload + scaling + power iteration + initial KKT

@@ -54,6 +54,8 @@ typedef struct rhp_options {
   int32_t use_graph;     /* 1: CUDA graph with a conditional WHILE node per block */
   int64_t block_limit;   /* max PDHG iterations per device block (default 64) */
   const void* nccl_id;   /* 128 bytes when world_size > 1, else NULL */
+  int32_t resident;      /* small-LP cluster-resident blocks: -1 auto, 0 off, 1 on */
+  int32_t pad_;
 } rhp_options;
 
 /* Step and restart parameters of the device loop. Derived quantities are

@@ -120,6 +120,8 @@ class RhpOptions(C.Structure):
         ("use_graph", C.c_int32),
         ("block_limit", C.c_int64),
         ("nccl_id", C.c_void_p),
+        ("resident", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -193,6 +195,7 @@ CUDA_SYMBOLS = [
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",
     "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_set_distributed",
+    "rhpdhg_set_resident",
     "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
@@ -279,6 +282,7 @@ def load_host() -> C.CDLL:
         sig = {
             "rhpdhg_set_device_options": [C.c_int, C.c_int, C.c_int64],
             "rhpdhg_set_distributed": [C.c_int, C.c_int, C.c_void_p],
+            "rhpdhg_set_resident": [C.c_int],
             "rhpdhg_session_create": [C.POINTER(LpView), C.POINTER(ConfigC), C.POINTER(P)],
             "rhpdhg_session_advance": [P, C.c_int64, C.POINTER(C.c_int32)],
             "rhpdhg_session_info": [P, c_int64_p, c_int64_p, C.POINTER(KktC), c_double_p,

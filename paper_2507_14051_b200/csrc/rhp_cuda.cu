@@ -21,6 +21,7 @@
 
 #include "layout.cuh"
 #include "pdhg_kernels.cuh"
+#include "resident.cuh"
 #include "scaling_kernels.cuh"
 #include "rhpdhg_cuda.h"
 
@@ -139,6 +140,11 @@ struct rhp_ctx {
   double* ypad = nullptr;        // [max_local]
   double* ygather = nullptr;     // [world * max_local]
   int64_t* agree = nullptr;      // 1 int64 for host-decision agreement
+  // small-LP cluster-resident blocks (resident.cuh)
+  bool resident = false;
+  int res_ctas = 1, res_wa = 1, res_wat = 1;
+  size_t res_smem = 0;
+  int32_t *res_a_split = nullptr, *res_at_split = nullptr;
 #ifdef RHP_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -352,6 +358,98 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s) {
   CK(cudaGetLastError());
 }
 
+// Contiguous split of an operator's rows into `parts` runs balanced by
+// nonzeros + rows.
+std::vector<int32_t> split_rows(const std::vector<int64_t>& rp, int parts) {
+  const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
+  std::vector<int32_t> s(static_cast<size_t>(parts) + 1, static_cast<int32_t>(rows));
+  s[0] = 0;
+  const double total = static_cast<double>(rp[rows] + rows);
+  int p = 1;
+  for (int64_t i = 0; i < rows && p < parts; ++i)
+    if (static_cast<double>(rp[i + 1] + i + 1) >= total * p / parts) s[p++] = static_cast<int32_t>(i + 1);
+  return s;
+}
+
+int lanes_for(int64_t nnz, int64_t rows) {
+  const int64_t mean = rows > 0 ? (nnz + rows - 1) / rows : 1;
+  return mean <= 4 ? 1 : mean <= 8 ? 2 : mean <= 16 ? 4 : mean <= 32 ? 8 : mean <= 64 ? 16 : 32;
+}
+
+// Shared-memory bytes of a CSR slice staged by the resident kernel.
+size_t slice_bytes(const std::vector<int64_t>& rp, int32_t r0, int32_t r1) {
+  const size_t rows = static_cast<size_t>(r1 - r0), nz = static_cast<size_t>(rp[r1] - rp[r0]);
+  auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+  return a16(4 * (rows + 1)) + a16(8 * nz) + a16(4 * nz);
+}
+
+// Chooses the cluster (up to 16 CTAs, one per SM) and row splits; false if
+// the per-CTA matrix slices do not fit in shared memory.
+bool setup_resident(rhp_ctx& c) {
+  const void* fn = reinterpret_cast<const void*>(k_resident);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kResSmemMax)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kResMaxCtas);
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = kResSmemMax;
+  int max_cluster = 1;
+  CK(cudaOccupancyMaxPotentialClusterSize(&max_cluster, fn, &cfg));
+  const int ctas = std::max(1, std::min(kResMaxCtas, max_cluster));
+  const std::vector<int32_t> sa = split_rows(c.L.A.rp, ctas);
+  const std::vector<int32_t> st = split_rows(c.L.At.rp, ctas);
+  size_t need = 0;
+  for (int r = 0; r < ctas; ++r)  // matrix slices + the shared-memory iterate slices
+    need = std::max(need, slice_bytes(c.L.A.rp, sa[r], sa[r + 1]) +
+                              slice_bytes(c.L.At.rp, st[r], st[r + 1]) +
+                              8 * (6 * static_cast<size_t>(sa[r + 1] - sa[r]) +
+                                   7 * static_cast<size_t>(st[r + 1] - st[r])));
+  if (need > kResSmemMax) return false;
+  c.res_ctas = ctas;
+  c.res_smem = std::max<size_t>(need, 16);
+  c.res_a_split = dev_alloc<int32_t>(sa.size());
+  c.res_at_split = dev_alloc<int32_t>(st.size());
+  upload(c.res_a_split, sa.data(), sa.size(), c.stream);
+  upload(c.res_at_split, st.data(), st.size(), c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  c.res_wa = lanes_for(c.L.nnz, c.m);
+  c.res_wat = lanes_for(c.L.nnz, c.n);
+  return true;
+}
+
+void launch_resident(rhp_ctx& c, cudaStream_t s) {
+  ResParams p{};
+  p.A = c.A.csr();
+  p.At = c.At.csr();
+  p.xp = c.xp;
+  p.yp = c.yp;
+  p.a_split = c.res_a_split;
+  p.at_split = c.res_at_split;
+  p.wa = c.res_wa;
+  p.wat = c.res_wat;
+  p.dual = epi_dual(c, 0);
+  p.aty = epi_aty(c, 0);
+  p.primal.ctl = c.ctl;
+  p.primal.o = primal_out(c);
+  const double* in[] = {c.aty, c.x, c.c, c.vl, c.vu, c.x0};
+  for (int k = 0; k < EpiPrimal::NIN; ++k) p.primal.in[k] = in[k];
+  p.ctl = c.ctl;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(c.res_ctas));
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = c.res_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(c.res_ctas);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_resident, p));
+}
+
 void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
   EpiPrimal e{};
   e.ctl = c.ctl;
@@ -537,6 +635,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     opt.world_size = 1;
     opt.use_graph = 1;
     opt.block_limit = 64;
+    opt.resident = -1;
     if (opt_in) opt = *opt_in;
     if (opt.block_limit < 1) opt.block_limit = 64;
     if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size)
@@ -634,6 +733,9 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       CK(cudaMemsetAsync(p2, 0, std::max<size_t>(m, 1) * sizeof(double), s));
     c->xchg = dev_alloc<double>(n + 16);
     CK(cudaStreamSynchronize(s));
+    // small LPs: one cluster runs whole blocks when its CSR slices fit in
+    // shared memory (auto) or when forced
+    c->resident = !c->dist && opt.resident != 0 && setup_resident(*c);
     if (c->dist) {
       c->ypad = dev_alloc<double>(static_cast<size_t>(c->max_local));
       c->ygather = dev_alloc<double>(static_cast<size_t>(c->max_local) * c->world);
@@ -669,6 +771,8 @@ int rhp_destroy(rhp_ctx* c) {
                     c->part3, c->partA, c->partAt, c->hist, c->xchg, c->ypad, c->ygather})
     if (p) cudaFree(p);
   if (c->agree) cudaFree(c->agree);
+  if (c->res_a_split) cudaFree(c->res_a_split);
+  if (c->res_at_split) cudaFree(c->res_at_split);
 #ifdef RHP_WITH_NCCL
   if (c->comm) ncclCommDestroy(c->comm);
 #endif
@@ -908,7 +1012,9 @@ int rhp_run_block(rhp_ctx* c, rhp_block_out* out) {
   return guarded([&] {
     cudaStream_t s = c->stream;
     CK(cudaEventRecord(c->ev0, s));
-    if (c->opt.use_graph) {
+    if (c->resident) {
+      launch_resident(*c, s);
+    } else if (c->opt.use_graph) {
       if (!c->graph_built) build_graph(*c);
       CK(cudaGraphLaunch(c->gexec, s));
     } else {

@@ -180,6 +180,10 @@ int rhpdhg_set_device_options(int device, int use_graph, int64_t block_limit) {
   });
 }
 
+int rhpdhg_set_resident(int mode) {
+  return guarded([&] { default_device_options().resident = mode < 0 ? -1 : (mode ? 1 : 0); });
+}
+
 int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id) {
   return guarded([&] {
     if (world_size < 1 || rank < 0 || rank >= world_size) throw UsageError("bad rank/world_size");

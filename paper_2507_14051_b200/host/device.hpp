@@ -64,6 +64,7 @@ inline rhp_options options(int device, bool use_graph, long block_limit) {
   o.use_graph = use_graph ? 1 : 0;
   o.block_limit = block_limit;
   o.nccl_id = nullptr;
+  o.resident = 0;  // per-op contexts (products, KKT, scaling) never use resident blocks
   return o;
 }
 
@@ -72,6 +73,7 @@ inline rhp_options options(int device, bool use_graph, long block_limit) {
 template <class DeviceOptionsT>
 inline rhp_options options(const DeviceOptionsT& d) {
   rhp_options o = options(d.device, d.use_graph, d.block_limit);
+  o.resident = d.resident;
   o.rank = d.rank;
   o.world_size = d.world_size;
   if (!d.nccl_id.empty()) {

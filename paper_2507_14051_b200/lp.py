@@ -372,6 +372,12 @@ def set_device_options(device: int = 0, use_graph: bool = True, block_limit: int
                  lib.rhpdhg_last_error().decode())
 
 
+def set_resident(mode: int = -1) -> None:
+    """Small-LP cluster-resident device blocks: -1 auto, 0 off, 1 on."""
+    lib = capi.load_host()
+    raise_status(lib.rhpdhg_set_resident(mode), lib.rhpdhg_last_error().decode())
+
+
 def nccl_unique_id() -> bytes:
     """rank 0: a fresh 128-byte ncclUniqueId to share with the other ranks."""
     lib = capi.load_cuda()

@@ -22,7 +22,8 @@ import torch.multiprocessing as mp
 import support
 from paper_2507_14051_b200 import LpProblem, SolverConfig, solve
 from paper_2507_14051_b200.generators import c1_small, random_rows_lp
-from paper_2507_14051_b200.lp import nccl_unique_id, partition_rows, set_distributed
+from paper_2507_14051_b200.lp import (nccl_unique_id, partition_rows, set_distributed,
+                                      set_resident)
 
 
 def block(lp: LpProblem, r0: int, r1: int) -> LpProblem:
@@ -127,12 +128,14 @@ def test_row_partition_exchange_matches_single_process_gloo():
 def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker):
     lp = maker()
     cfg = SolverConfig(epsilon=1e-7, record_residual_history=True)
-    single = solve(lp, cfg)
     try:
+        set_resident(0)  # compare against the multi-CTA single-GPU path
+        single = solve(lp, cfg)
         set_distributed(0, 1, nccl_unique_id())
         part = solve(lp, cfg)
     finally:
         set_distributed(0, 1, None)
+        set_resident(-1)
     assert part.status == single.status
     assert part.iterations == single.iterations and part.restart_count == single.restart_count
     assert part.objective == single.objective

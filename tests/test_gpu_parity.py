@@ -193,6 +193,36 @@ def test_graph_and_plain_launch_modes_agree_bitwise(gpu):
         assert np.array_equal(r.fixed_point_residual_history, a.fixed_point_residual_history)
 
 
+@pytest.mark.parametrize("mode", [0, 1], ids=["multi_cta", "cluster_resident"])
+def test_both_block_engines_match_oracle(gpu, mode):
+    """The multi-CTA K1/K2 path and the small-LP cluster-resident block
+    kernel each reproduce the reference solve (objective 1e-6, KKT at eps)
+    and the first iterates (1e-10)."""
+    from paper_2507_14051_b200.lp import set_resident
+
+    lp = c1_small(m=300, n=500)
+    try:
+        set_resident(mode)
+        for eps in (1e-4, 1e-8):
+            cfg = SolverConfig(epsilon=eps)
+            g = solve(lp, cfg)
+            o = support.solve_with(support.oracle(), lp, cfg)
+            assert g.status == o.status == "optimal"
+            assert abs(g.objective - o.objective) <= 1e-6 * max(1.0, abs(o.objective))
+            k = support.kkt_with(support.oracle(), lp, g.x, g.y)
+            assert k["gap_rel"] <= eps and k["primal_rel"] <= eps
+        for it in (1, 5, 30, 64, 100):
+            cfg = SolverConfig(epsilon=1e-300, iteration_limit=it)
+            g = solve(lp, cfg)
+            o = support.solve_with(support.oracle(), lp, cfg)
+            assert max_rel(g.x, o.x) <= 1e-10 and max_rel(g.y, o.y) <= 1e-10
+        a = solve(lp, SolverConfig(epsilon=1e-8, record_residual_history=True))
+        b = solve(lp, SolverConfig(epsilon=1e-8, record_residual_history=True))
+        assert np.array_equal(a.x, b.x) and a.iterations == b.iterations  # deterministic
+    finally:
+        set_resident(-1)
+
+
 def test_operator_budget_and_counters(gpu):
     lp = support.lp_from_json(RANDOM[1]["lp"])
     r = solve(lp, SolverConfig(epsilon=1e-6))

@@ -38,6 +38,13 @@ namespace rhp {
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Epilogue per-row inputs: staged by TMA with the tile (1) or loaded by the
+// row's thread into registers at tile start, overlapping the gather (0).
+#ifndef RHP_EPI_TMA
+#define RHP_EPI_TMA 1
+#endif
+constexpr bool kEpiTma = RHP_EPI_TMA != 0;
+
 // Shared-memory layout of one pipeline stage for an epilogue with NIN
 // per-row input vectors. Offsets keep every TMA destination 16-B aligned;
 // the +2/+8/+4 slack absorbs the 16-B alignment of the copied source ranges.
@@ -80,14 +87,16 @@ __device__ __forceinline__ void issue_tile(const Csr& A, const Epi& epi, const T
   const uint32_t bv = static_cast<uint32_t>(8 * (ve - vb));
   const uint32_t bi = static_cast<uint32_t>(4 * (ie - ib));
   const uint32_t br = static_cast<uint32_t>(8 * (re - rb));
-  const uint32_t bx = static_cast<uint32_t>(8 * (xe - xb));
+  const uint32_t bx = kEpiTma ? static_cast<uint32_t>(8 * (xe - xb)) : 0u;
   mbar_arrive_expect_tx(bar, bv + bi + br + bx * Epi::NIN);
   if (bv) tma_load_1d(stage + L::off_vals, A.v + vb, bv, bar);
   if (bi) tma_load_1d(stage + L::off_idx, A.ci + ib, bi, bar);
   tma_load_1d(stage + L::off_rp, A.rp + rb, br, bar);
+  if constexpr (kEpiTma) {
 #pragma unroll
-  for (int k = 0; k < Epi::NIN; ++k)
-    tma_load_1d(stage + L::off_in + 8 * size_t(L::kIn) * k, epi.in[k] + xb, bx, bar);
+    for (int k = 0; k < Epi::NIN; ++k)
+      tma_load_1d(stage + L::off_in + 8 * size_t(L::kIn) * k, epi.in[k] + xb, bx, bar);
+  }
 }
 
 template <int W>
@@ -130,6 +139,15 @@ __device__ __forceinline__ void compute_tile(const double* __restrict__ xg, cons
   const int* idx = reinterpret_cast<const int*>(stage + L::off_idx) + (d.b & 3);
   const int64_t* rps = reinterpret_cast<const int64_t*>(stage + L::off_rp) + (d.r0 & 1);
   const double* ein = reinterpret_cast<const double*>(stage + L::off_in) + (d.r0 & 1);
+  // register path: the row's epilogue inputs, loaded now, used in (3)
+  constexpr int NI = Epi::NIN > 0 ? Epi::NIN : 1;
+  double ereg[NI];
+  if constexpr (!kEpiTma) {
+    if (threadIdx.x < rows) {
+#pragma unroll
+      for (int k = 0; k < Epi::NIN; ++k) ereg[k] = epi.in[k][d.r0 + threadIdx.x];
+    }
+  }
   // (1) products in place. All indices and all x gathers of a thread are
   // loaded into registers before the first shared-memory store, so the
   // kTileNnz/kBlock gathers are in flight together (an interleaved
@@ -163,7 +181,12 @@ __device__ __forceinline__ void compute_tile(const double* __restrict__ xg, cons
   }
   __syncthreads();
   // (3) epilogue, thread per row
-  if (threadIdx.x < rows) epi.row(d.r0 + threadIdx.x, rowsum[threadIdx.x], ein + threadIdx.x, L::kIn, acc);
+  if (threadIdx.x < rows) {
+    if constexpr (kEpiTma)
+      epi.row(d.r0 + threadIdx.x, rowsum[threadIdx.x], ein + threadIdx.x, L::kIn, acc);
+    else
+      epi.row(d.r0 + threadIdx.x, rowsum[threadIdx.x], ereg, 1, acc);
+  }
 }
 
 template <class Epi>

@@ -32,7 +32,7 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kMinBlocks = RHP_MIN_BLOCKS;  // resident CTAs per SM the SpMV is built for
 constexpr int kTileNnz = RHP_TILE_NNZ;      // nonzeros per stream tile
 constexpr int kTileRows = kBlock;    // rows per stream tile at most (one per thread)
-constexpr int64_t kChunkNnz = 8192;  // nonzeros per chunk tile of a long row
+constexpr int64_t kChunkNnz = 4096;  // nonzeros per chunk tile of a long row
 
 // std::max / std::min semantics (first argument wins on ties and NaN), which
 // the reference's projections rely on (lp_problem.cpp:62, pdhg.cpp:44,54).

@@ -270,13 +270,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
   __shared__ TileDesc sdesc[2];  // descriptor of the tile in each stage
   const int64_t grid = gridDim.x;
-  int64_t t = blockIdx.x;
+  // Tile order: the chunk tiles of long rows first (longest work first, so
+  // they do not form a tail), then the stream tiles. CTA b takes tiles
+  // b, b+grid, ...; t below indexes stream tiles only.
+  const int64_t n_chunks = s.total_tiles - s.n_stream;
+  int64_t tc = blockIdx.x;
+  int64_t t = tc;
+  if (t < n_chunks) t += ((n_chunks - t + grid - 1) / grid) * grid;
+  t -= n_chunks;
   TileDesc next{}, after{};
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
-    if (t < s.n_stream) {
+    if (t < s.n_stream) {  // the first stream tile streams in while chunks run
       sdesc[0] = load_desc(s, t);
       issue_tile(A, epi, sdesc[0], smem, &bars[0]);
     }
@@ -284,6 +291,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
     if (t + 2 * grid < s.n_stream) after = load_desc(s, t + 2 * grid);
   }
   __syncthreads();
+  for (; tc < n_chunks; tc += grid) tile_chunk(A, xg, s, tc, epi, acc);
   for (int it = 0; t < s.n_stream; t += grid, ++it) {
     const int st = it & 1;
     if (threadIdx.x == 0) {
@@ -300,7 +308,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
     compute_tile(xg, d, smem + st * L::bytes, epi, acc, rowsum);
     __syncthreads();  // stage st is free for the copy issued next iteration
   }
-  for (; t < s.total_tiles; t += grid) tile_chunk(A, xg, s, t - s.n_stream, epi, acc);
   if constexpr (Epi::REDUCE) {
     block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
     if constexpr (Epi::FINAL) {
@@ -325,14 +332,16 @@ __global__ void __launch_bounds__(kBlock) epilogue_walk(Sched s, Epi epi, double
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
   double ein[Epi::NIN > 0 ? Epi::NIN : 1];
+  const int64_t n_chunks = s.total_tiles - s.n_stream;  // same order as spmv_fused
   for (int64_t tile = blockIdx.x; tile < s.total_tiles; tile += gridDim.x) {
     int64_t row = -1;
     int slot = -1;
-    if (tile < s.n_stream) {
-      const int64_t r0 = s.tile_row[tile], r1 = s.tile_row_end[tile];
+    if (tile >= n_chunks) {
+      const int64_t ts = tile - n_chunks;
+      const int64_t r0 = s.tile_row[ts], r1 = s.tile_row_end[ts];
       if (r0 + threadIdx.x < r1) row = r0 + threadIdx.x;
     } else if (threadIdx.x == 0) {
-      const int64_t chunk = tile - s.n_stream;
+      const int64_t chunk = tile;
       slot = s.chunk_slot[chunk];
       if (slot < 0 || chunk == s.chunk_first[chunk]) row = s.chunk_row[chunk];
     }

@@ -19,20 +19,24 @@ namespace rhp {
 
 constexpr int kBlock = 256;          // threads per CTA for every hot kernel
 constexpr int kWarps = kBlock / 32;
-// 1024 nonzeros (4 per thread) x 3 resident CTAs per SM measured best for the
-// fused iteration kernels on B200 (C2: 5.18k iter/s vs 4.92k for 2048x2,
-// 4.82k for 2048x3, 4.62k for 1024x4 whose 224 KB of shared memory leaves
-// almost no L1; plain-SpMV probe in tools/spmv_probe.py)
-#ifndef RHP_TILE_NNZ
-#define RHP_TILE_NNZ 1024
+// SpMV engine (spmv.cuh): every warp owns one contiguous merge-path range of
+// its operator and walks it in windows of kWin = 32 * kPer nonzeros.
+#ifndef RHP_WIN_PER
+#define RHP_WIN_PER 8
 #endif
 #ifndef RHP_MIN_BLOCKS
-#define RHP_MIN_BLOCKS 3
+#define RHP_MIN_BLOCKS 2
 #endif
 constexpr int kMinBlocks = RHP_MIN_BLOCKS;  // resident CTAs per SM the SpMV is built for
-constexpr int kTileNnz = RHP_TILE_NNZ;      // nonzeros per stream tile
-constexpr int kTileRows = kBlock;    // rows per stream tile at most (one per thread)
-constexpr int64_t kChunkNnz = 4096;  // nonzeros per chunk tile of a long row
+constexpr int kPer = RHP_WIN_PER;           // nonzeros per lane per window
+constexpr int kWin = 32 * kPer;             // nonzeros per warp window
+static_assert(kPer == 4 || kPer == 8, "window of 4 or 8 nonzeros per lane");
+// Cost of a row in nonzeros when balancing warp ranges (row pointer, flags,
+// epilogue inputs and outputs vs index, value and gather per nonzero).
+#ifndef RHP_ROW_WEIGHT
+#define RHP_ROW_WEIGHT 3.0
+#endif
+constexpr double kRowWeight = RHP_ROW_WEIGHT;
 
 // std::max / std::min semantics (first argument wins on ties and NaN), which
 // the reference's projections rely on (lp_problem.cpp:62, pdhg.cpp:44,54).
@@ -99,26 +103,28 @@ struct Ctl {
   double* hist;                    // [block_limit] residual history of the current block
 };
 
-// Operator schedule (built by layout.cu): n_stream stream tiles (runs of
-// consecutive rows with <= kTileNnz nonzeros and <= kTileRows rows), then one
-// chunk tile per <= kChunkNnz slice of every row longer than kTileNnz.
+// Operator schedule (built by layout.cu for a given warp count): warp w owns
+// the merge-path range that starts at row warp_row[w], nonzero warp_nz[w]
+// and ends where warp w+1 starts (rows + nonzeros balanced, boundaries snapped
+// to row starts except inside long rows). A row cut by one or more range
+// boundaries is a "split row" with a slot: every warp that touches it stores
+// its partial sum, and the last one to arrive adds them in warp order and runs
+// the row's epilogue (reductions into long_red[slot]).
 struct Sched {
-  int32_t n_multi;            // rows split across several chunks
-  int32_t pad;
-  int64_t n_stream;
-  int64_t total_tiles;        // n_stream + chunks
-  const int32_t* tile_row;    // [n_stream] first row of the tile
-  const int32_t* tile_row_end;// [n_stream] one past its last row
-  const int64_t* tile_nz;     // [2*n_stream] nonzero range [b, e) of the tile
-  const int32_t* chunk_row;   // [chunks] row
-  const int64_t* chunk_beg;   // [chunks]
-  const int64_t* chunk_end;   // [chunks]
-  const int32_t* chunk_first; // [chunks] first chunk of the same row
-  const int32_t* chunk_count; // [chunks] chunks of the same row
-  const int32_t* chunk_slot;  // [chunks] multi-chunk slot or -1
-  double* chunk_part;         // [chunks]
+  int32_t n_multi;            // split rows (slots)
+  int32_t n_warps;            // warps the ranges were built for (grid * kWarps)
+  int64_t rows;
+  const int64_t* rp;          // the operator's row pointers
+  const int64_t* warp_row;    // [n_warps + 1]
+  const int64_t* warp_nz;     // [n_warps + 1]
+  const int32_t* head_slot;   // [n_warps] slot of warp_row[w] when the range starts inside it, else -1
+  const int32_t* tail_slot;   // [n_warps] slot of the row the range ends inside, else -1
+  const int64_t* slot_row;    // [n_multi]
+  const int32_t* slot_first;  // [n_multi] first contributing warp (it holds the row's start)
+  const int32_t* slot_count;  // [n_multi] contributing warps (consecutive)
+  double* slot_part;          // [2 * n_warps] per warp: head partial, tail partial
   unsigned int* slot_ticket;  // [n_multi]
-  double* long_red;           // [n_multi * 16] epilogue reductions of multi-chunk rows
+  double* long_red;           // [n_multi * 16] epilogue reductions of split rows
 };
 
 struct Csr {
@@ -179,19 +185,29 @@ __device__ __forceinline__ void block_sum_partials(const double* part, int count
   __syncthreads();
 }
 
-// Adds the epilogue reductions of multi-chunk long rows (fixed slot order).
+// Adds the epilogue reductions of split rows: block-parallel, fixed order
+// (thread-strided sums, then the fixed block tree of block_sum_partials).
 template <int N>
 __device__ __forceinline__ void add_slots(const double* long_red, int n_multi, double (&out)[N]) {
   if (n_multi == 0) return;
-  __shared__ double sm[N];
-  if (threadIdx.x < N) {
+  __shared__ double sm[N][kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
     double v = 0.0;
-    for (int i = 0; i < n_multi; ++i) v += __ldcg(long_red + (size_t)i * 16 + threadIdx.x);
-    sm[threadIdx.x] = v;
+    for (int i = threadIdx.x; i < n_multi; i += kBlock) v += __ldcg(long_red + (size_t)i * 16 + q);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) sm[q][warp] = v;
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < N; ++q) out[q] += sm[q];
+  for (int q = 0; q < N; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += sm[q][w];
+    out[q] += s;
+  }
   __syncthreads();
 }
 

@@ -1,4 +1,4 @@
-// layout.cu — host-side build of the device layout and tile schedules
+// layout.cu — host-side build of the device layout and warp schedules
 // (see layout.cuh). Host code only; compiled by nvcc with the device library.
 #include <algorithm>
 #include <cmath>
@@ -9,60 +9,82 @@
 
 namespace rhp {
 
-// Greedy nnz-balanced tiling in row order: a stream tile grows while it has
-// <= kTileNnz nonzeros and <= kTileRows rows; a row longer than kTileNnz
-// closes the current tile and is cut into chunk tiles of <= kChunkNnz.
-void build_schedule(HostOperator& op) {
-  op.tile_row.clear();
-  op.tile_row_end.clear();
-  op.tile_nz.clear();
-  op.chunk_row.clear();
-  op.chunk_beg.clear();
-  op.chunk_end.clear();
-  op.chunk_first.clear();
-  op.chunk_count.clear();
-  op.chunk_slot.clear();
+// Merge-path warp ranges (Sched in device_common.cuh). Boundary k sits at
+// cost k * total / W, cost(r, e) = e + row_weight * r; it snaps to the nearer
+// row start unless the row is longer than the snap length, in which case the
+// row is split there. Consecutive boundaries inside one row share its slot.
+void build_schedule(HostOperator& op, int64_t n_warps, double row_weight) {
+  const int64_t W = std::max<int64_t>(1, n_warps);
+  const int64_t R = op.rows, Z = op.nnz;
+  const std::vector<int64_t>& rp = op.rp;
   for (int k = 0; k < 8; ++k) op.bin_rows[k] = 0;
-  int32_t n_multi = 0;
-  int64_t r = 0;
-  while (r < op.rows) {
-    const int64_t L = op.rp[r + 1] - op.rp[r];
-    op.bin_rows[row_kind(L)]++;
-    if (L > kTileNnz) {
-      const int64_t b = op.rp[r], e = op.rp[r + 1];
-      const int64_t nch = (e - b + kChunkNnz - 1) / kChunkNnz;
-      const int32_t first = static_cast<int32_t>(op.chunk_row.size());
-      const int32_t slot = nch > 1 ? n_multi++ : -1;
-      for (int64_t c = 0; c < nch; ++c) {
-        op.chunk_row.push_back(static_cast<int32_t>(r));
-        op.chunk_beg.push_back(b + c * kChunkNnz);
-        op.chunk_end.push_back(std::min(e, b + (c + 1) * kChunkNnz));
-        op.chunk_first.push_back(first);
-        op.chunk_count.push_back(static_cast<int32_t>(nch));
-        op.chunk_slot.push_back(slot);
+  for (int64_t r = 0; r < R; ++r) op.bin_rows[row_kind(rp[r + 1] - rp[r])]++;
+  op.warp_row.assign(static_cast<size_t>(W) + 1, R);
+  op.warp_nz.assign(static_cast<size_t>(W) + 1, Z);
+  op.warp_row[0] = 0;
+  op.warp_nz[0] = 0;
+  const double total = static_cast<double>(Z) + row_weight * static_cast<double>(R);
+  const double per = total / static_cast<double>(W);
+  const int64_t snap = std::max<int64_t>(1, std::min<int64_t>(2 * kWin, static_cast<int64_t>(per / 2)));
+  auto cost = [&](int64_t r) { return static_cast<double>(rp[r]) + row_weight * static_cast<double>(r); };
+  int64_t pr = 0, pe = 0;
+  for (int64_t k = 1; k < W; ++k) {
+    const double T = per * static_cast<double>(k);
+    // last row r with cost(r) <= T
+    int64_t lo = 0, hi = R;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (cost(mid) <= T) lo = mid;
+      else hi = mid - 1;
+    }
+    int64_t r = lo, e = R > 0 ? rp[lo] : 0;
+    if (r < R) {
+      const int64_t len = rp[r + 1] - rp[r];
+      if (len <= snap) {
+        if (T - cost(r) > cost(r + 1) - T) ++r;
+        e = rp[r];
+      } else {
+        const double off = T - cost(r) - row_weight;
+        const int64_t j = off <= 0 ? 0 : std::min<int64_t>(len, static_cast<int64_t>(off));
+        e = rp[r] + j;
+        if (j == len) {
+          ++r;
+          e = rp[r];
+        }
       }
-      ++r;
-      continue;
     }
-    const int64_t r0 = r;
-    int64_t nz = 0;
-    while (r < op.rows && r - r0 < kTileRows) {
-      const int64_t len = op.rp[r + 1] - op.rp[r];
-      if (len > kTileNnz || nz + len > kTileNnz) break;
-      if (r > r0) op.bin_rows[row_kind(len)]++;
-      nz += len;
-      ++r;
+    if (e < pe || (e == pe && r < pr)) {  // keep boundaries monotone
+      r = pr;
+      e = pe;
     }
-    op.tile_row.push_back(static_cast<int32_t>(r0));
-    op.tile_row_end.push_back(static_cast<int32_t>(r));
-    op.tile_nz.push_back(op.rp[r0]);
-    op.tile_nz.push_back(op.rp[r]);
+    op.warp_row[k] = r;
+    op.warp_nz[k] = e;
+    pr = r;
+    pe = e;
+  }
+  op.head_slot.assign(static_cast<size_t>(W), -1);
+  op.tail_slot.assign(static_cast<size_t>(W), -1);
+  op.slot_row.clear();
+  op.slot_first.clear();
+  op.slot_count.clear();
+  for (int64_t k = 1; k < W; ++k) {
+    const int64_t r = op.warp_row[k], e = op.warp_nz[k];
+    if (r >= R || e <= rp[r]) continue;  // boundary at a row start
+    if (op.slot_row.empty() || op.slot_row.back() != r) {
+      op.slot_row.push_back(r);
+      op.slot_first.push_back(static_cast<int32_t>(k - 1));
+      op.slot_count.push_back(0);
+    }
+    const int32_t sl = static_cast<int32_t>(op.slot_row.size()) - 1;
+    op.slot_count[sl] = static_cast<int32_t>(k - op.slot_first[sl] + 1);
+    op.head_slot[k] = sl;
+    op.tail_slot[k - 1] = sl;
   }
   Sched& s = op.sched;
   s = Sched{};
-  s.n_multi = n_multi;
-  s.n_stream = static_cast<int64_t>(op.tile_row.size());
-  s.total_tiles = s.n_stream + static_cast<int64_t>(op.chunk_row.size());
+  s.n_multi = static_cast<int32_t>(op.slot_row.size());
+  s.n_warps = static_cast<int32_t>(W);
+  s.rows = R;
 }
 
 std::vector<int64_t> partition_rows(const rhpdhg_lp_view& lp, int world_size) {
@@ -164,9 +186,6 @@ void build_layout(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end, 
   L.icol.resize(static_cast<size_t>(n));
   for (int64_t c = 0; c < n; ++c) L.pcol[c] = L.icol[c] = static_cast<int32_t>(c);
 
-  // (4) tile schedules
-  build_schedule(A);
-  build_schedule(T);
 }
 
 }  // namespace rhp

@@ -7,7 +7,8 @@
 // elements of every row in the reference's order (ascending column for A,
 // ascending row for A^T), so sequential per-row sums match the reference
 // bit-for-bit where the kernels sum sequentially (scaling, short rows).
-// Each operator gets an nnz-balanced tile schedule (spmv.cuh).
+// Each operator gets a merge-path warp schedule (spmv.cuh) once the grid is
+// known (build_schedule).
 //
 // The permutation maps (prow/pcol) are kept in the interface for layouts
 // that reorder rows; the current layout is the identity.
@@ -30,7 +31,7 @@ inline int row_kind(int64_t L) {
   if (L <= 32) return 3;
   if (L <= 64) return 4;
   if (L <= 512) return 5;
-  if (L <= kTileNnz) return 6;
+  if (L <= 1024) return 6;
   return 7;
 }
 
@@ -40,10 +41,9 @@ struct HostOperator {
   std::vector<int32_t> ci;
   std::vector<double> v;
   Sched sched{};  // host copy; device pointers filled at upload
-  std::vector<int32_t> tile_row, tile_row_end;
-  std::vector<int64_t> tile_nz;  // [2 * tiles]: nonzero range of each stream tile
-  std::vector<int32_t> chunk_row, chunk_first, chunk_count, chunk_slot;
-  std::vector<int64_t> chunk_beg, chunk_end;
+  // warp schedule (Sched in device_common.cuh)
+  std::vector<int64_t> warp_row, warp_nz, slot_row;
+  std::vector<int32_t> head_slot, tail_slot, slot_first, slot_count;
   int64_t bin_rows[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // rows per length class
 };
 
@@ -65,8 +65,10 @@ struct HostLayout {
 // duplicate/unsorted entry), std::invalid_argument (too large).
 void build_layout(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end, HostLayout& out);
 
-// The tile schedule of one operator (exposed for tests via rhp_plan).
-void build_schedule(HostOperator& op);
+// Merge-path warp schedule of one operator for n_warps warps: ranges
+// balanced by nonzeros + row_weight * rows, boundaries snapped to row starts
+// except inside rows longer than the snap length.
+void build_schedule(HostOperator& op, int64_t n_warps, double row_weight);
 
 // Balanced contiguous row partition by nonzeros: returns
 // world_size+1 row offsets.

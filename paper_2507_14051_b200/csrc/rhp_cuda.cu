@@ -91,10 +91,9 @@ struct DevOp {
   double* v = nullptr;       // current values (original, then scaled)
   double* v_orig = nullptr;  // original values, kept until scaling is done
   Sched sched{};             // with device pointers
-  int32_t *chunk_row = nullptr, *chunk_first = nullptr, *chunk_count = nullptr,
-          *chunk_slot = nullptr, *tile_row = nullptr, *tile_row_end = nullptr;
-  int64_t *chunk_beg = nullptr, *chunk_end = nullptr, *tile_nz = nullptr;
-  double *chunk_part = nullptr, *long_red = nullptr;
+  int64_t *warp_row = nullptr, *warp_nz = nullptr, *slot_row = nullptr;
+  int32_t *head_slot = nullptr, *tail_slot = nullptr, *slot_first = nullptr, *slot_count = nullptr;
+  double *slot_part = nullptr, *long_red = nullptr;
   unsigned int* slot_ticket = nullptr;
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
@@ -169,53 +168,48 @@ void upload_op(DevOp& d, const HostOperator& h, cudaStream_t s) {
   upload(d.ci, h.ci.data(), h.ci.size(), s);
   upload(d.v, h.v.data(), h.v.size(), s);
   upload(d.v_orig, h.v.data(), h.v.size(), s);
-  const size_t nt = h.tile_row.size();
-  d.tile_row = dev_alloc<int32_t>(nt);
-  d.tile_row_end = dev_alloc<int32_t>(nt);
-  upload(d.tile_row, h.tile_row.data(), nt, s);
-  upload(d.tile_row_end, h.tile_row_end.data(), nt, s);
-  d.tile_nz = dev_alloc<int64_t>(2 * nt);
-  upload(d.tile_nz, h.tile_nz.data(), 2 * nt, s);
-  const size_t nch = h.chunk_row.size();
-  d.chunk_row = dev_alloc<int32_t>(nch);
-  d.chunk_first = dev_alloc<int32_t>(nch);
-  d.chunk_count = dev_alloc<int32_t>(nch);
-  d.chunk_slot = dev_alloc<int32_t>(nch);
-  d.chunk_beg = dev_alloc<int64_t>(nch);
-  d.chunk_end = dev_alloc<int64_t>(nch);
-  d.chunk_part = dev_alloc<double>(nch);
-  upload(d.chunk_row, h.chunk_row.data(), nch, s);
-  upload(d.chunk_first, h.chunk_first.data(), nch, s);
-  upload(d.chunk_count, h.chunk_count.data(), nch, s);
-  upload(d.chunk_slot, h.chunk_slot.data(), nch, s);
-  upload(d.chunk_beg, h.chunk_beg.data(), nch, s);
-  upload(d.chunk_end, h.chunk_end.data(), nch, s);
-  const size_t nm = static_cast<size_t>(h.sched.n_multi);
-  d.slot_ticket = dev_alloc<unsigned int>(nm);
-  d.long_red = dev_alloc<double>(std::max<size_t>(nm, 1) * 16);
-  CK(cudaMemsetAsync(d.slot_ticket, 0, std::max<size_t>(nm, 1) * sizeof(unsigned int), s));
-  CK(cudaMemsetAsync(d.long_red, 0, std::max<size_t>(nm, 1) * 16 * sizeof(double), s));
+}
+
+// Uploads the warp schedule of an operator (built for the operator's grid).
+void upload_sched(DevOp& d, const HostOperator& h, cudaStream_t s) {
+  const size_t W = static_cast<size_t>(h.sched.n_warps), ns = h.slot_row.size();
+  d.warp_row = dev_alloc<int64_t>(W + 1);
+  d.warp_nz = dev_alloc<int64_t>(W + 1);
+  d.head_slot = dev_alloc<int32_t>(W);
+  d.tail_slot = dev_alloc<int32_t>(W);
+  d.slot_part = dev_alloc<double>(2 * W);
+  upload(d.warp_row, h.warp_row.data(), W + 1, s);
+  upload(d.warp_nz, h.warp_nz.data(), W + 1, s);
+  upload(d.head_slot, h.head_slot.data(), W, s);
+  upload(d.tail_slot, h.tail_slot.data(), W, s);
+  d.slot_row = dev_alloc<int64_t>(ns);
+  d.slot_first = dev_alloc<int32_t>(ns);
+  d.slot_count = dev_alloc<int32_t>(ns);
+  upload(d.slot_row, h.slot_row.data(), ns, s);
+  upload(d.slot_first, h.slot_first.data(), ns, s);
+  upload(d.slot_count, h.slot_count.data(), ns, s);
+  d.slot_ticket = dev_alloc<unsigned int>(std::max<size_t>(ns, 1));  // zeroed by dev_alloc
+  d.long_red = dev_alloc<double>(std::max<size_t>(ns, 1) * 16);
   d.sched = h.sched;
-  d.sched.tile_row = d.tile_row;
-  d.sched.tile_row_end = d.tile_row_end;
-  d.sched.tile_nz = d.tile_nz;
-  d.sched.chunk_row = d.chunk_row;
-  d.sched.chunk_beg = d.chunk_beg;
-  d.sched.chunk_end = d.chunk_end;
-  d.sched.chunk_first = d.chunk_first;
-  d.sched.chunk_count = d.chunk_count;
-  d.sched.chunk_slot = d.chunk_slot;
-  d.sched.chunk_part = d.chunk_part;
+  d.sched.rp = d.rp;
+  d.sched.warp_row = d.warp_row;
+  d.sched.warp_nz = d.warp_nz;
+  d.sched.head_slot = d.head_slot;
+  d.sched.tail_slot = d.tail_slot;
+  d.sched.slot_row = d.slot_row;
+  d.sched.slot_first = d.slot_first;
+  d.sched.slot_count = d.slot_count;
+  d.sched.slot_part = d.slot_part;
   d.sched.slot_ticket = d.slot_ticket;
   d.sched.long_red = d.long_red;
+  CK(cudaStreamSynchronize(s));
 }
 
 void free_op(DevOp& d) {
-  for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.chunk_row,
-                  (void*)d.chunk_first, (void*)d.chunk_count, (void*)d.chunk_slot,
-                  (void*)d.chunk_beg, (void*)d.chunk_end, (void*)d.chunk_part,
-                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.tile_row,
-                  (void*)d.tile_row_end, (void*)d.tile_nz})
+  for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.warp_row,
+                  (void*)d.warp_nz, (void*)d.slot_row, (void*)d.head_slot, (void*)d.tail_slot,
+                  (void*)d.slot_first, (void*)d.slot_count, (void*)d.slot_part,
+                  (void*)d.long_red, (void*)d.slot_ticket})
     if (p) cudaFree(p);
   d = DevOp{};
 }
@@ -255,20 +249,16 @@ template <class Epi>
 void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
                  double* part, unsigned int* ticket, cudaStream_t s) {
   (void)c;
-  spmv_fused<Epi><<<grid, kBlock, spmv_smem_bytes<Epi::NIN>(), s>>>(op.csr(), xg, op.sched, epi,
-                                                                   part, ticket);
+  spmv_fused<Epi><<<grid, kBlock, 0, s>>>(op.csr(), xg, op.sched, epi, part, ticket);
   CK(cudaGetLastError());
 }
 
-// Opt the SpMV instantiations into their dynamic shared memory and return the
-// resident CTAs per SM.
+// Resident CTAs per SM of an SpMV instantiation.
 template <class Epi>
 int prepare_spmv() {
   const void* fn = reinterpret_cast<const void*>(spmv_fused<Epi>);
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(spmv_smem_bytes<Epi::NIN>())));
   int b = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, spmv_smem_bytes<Epi::NIN>()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
   if (b < 1) throw CudaError("spmv kernel does not fit on an SM");
   return b;
 }
@@ -705,11 +695,17 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
                                 prepare_spmv<EpiKktRowDist>(), occ_store});
     const int occ_at = std::min({prepare_spmv<EpiAty>(), prepare_spmv<EpiKktCol>(),
                                  prepare_spmv<EpiPowerW>(), occ_store});
-    auto clampg = [](int64_t tiles, int64_t cap) {
-      return static_cast<int>(std::max<int64_t>(1, std::min(tiles, cap)));
+    // at least ~2 windows of work per warp, at most every resident CTA
+    auto clampg = [](const HostOperator& h, int64_t cap) {
+      const int64_t work = h.nnz + 2 * h.rows;
+      return static_cast<int>(std::max<int64_t>(1, std::min(cap, work / (2 * kWin * kWarps))));
     };
-    c->grid_a = clampg(c->A.sched.total_tiles, (int64_t)c->sm_count * occ_a);
-    c->grid_at = clampg(c->At.sched.total_tiles, (int64_t)c->sm_count * occ_at);
+    c->grid_a = clampg(c->L.A, (int64_t)c->sm_count * occ_a);
+    c->grid_at = clampg(c->L.At, (int64_t)c->sm_count * occ_at);
+    build_schedule(c->L.A, (int64_t)c->grid_a * kWarps, kRowWeight);
+    build_schedule(c->L.At, (int64_t)c->grid_at * kWarps, kRowWeight);
+    upload_sched(c->A, c->L.A, s);
+    upload_sched(c->At, c->L.At, s);
     c->grid_vec = vec_grid(*c, std::max<int64_t>(c->m, c->n));
     c->grid_max = std::max({c->grid_a, c->grid_at, c->grid_vec});
     for (double** p2 : {&c->part1, &c->part3, &c->partA, &c->partAt})

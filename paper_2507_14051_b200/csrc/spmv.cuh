@@ -1,5 +1,5 @@
-// spmv.cuh — nnz-balanced fp64 CSR SpMV with TMA-staged tiles and a fused
-// per-row epilogue.
+// spmv.cuh — warp-autonomous merge-path fp64 CSR SpMV with a fused per-row
+// epilogue.
 //
 // Replaces SparseMatrix::multiply / multiply_transpose
 // (/root/reference/proj/src/sparse_matrix.cpp:67-87). Both A and A^T are
@@ -7,307 +7,254 @@
 // product needs atomics and every output row is produced in a fixed order
 // (deterministic).
 //
-// Tiles (built on the host, layout.cu):
-//   stream tile: a run of consecutive rows holding <= kTileNnz nonzeros and
-//     <= kTileRows rows.
-//   chunk tile: one CTA per <= kChunkNnz slice of a row longer than
-//     kTileNnz; a row of several chunks is completed by the last chunk to
-//     land (fixed-order sum of the chunk partials).
-// A persistent grid walks the tiles with a static stride, so each CTA's
-// reduction partials have a fixed composition.
+// Work split (layout.cu, build_schedule): warp w of the persistent grid owns
+// one contiguous merge-path range of the operator — rows + nonzeros balanced
+// across all warps, boundaries at row starts except inside long rows. A warp
+// never synchronises with the other warps of its CTA while it walks its
+// range; the only CTA barriers are in the final reduction of the epilogue
+// sums.
 //
-// Stream tiles are double-buffered through shared memory by the bulk-copy
-// engine: while the CTA computes tile i from stage i&1, one thread has
-// already issued cp.async.bulk copies of tile i+1's values, column indices,
-// row pointers and the epilogue's per-row input vectors (y, ax, bounds,
-// anchor, ...) into stage (i+1)&1, completing on an mbarrier. Tile
-// descriptors are loaded two tiles ahead, so issuing never waits on memory.
-// Compute per tile, all from shared memory except the x gather:
-//   (1) products v*x[c] in place (x through the read-only path, L2 resident),
-//   (2) row sums by groups of W lanes (W from the tile's mean row length;
-//       fixed per tile, so the order is deterministic; W = 1 is the
-//       reference's sequential order),
-//   (3) the epilogue, one thread per row, inputs from the stage, outputs
-//       stored straight to global memory (coalesced).
+// Per window of kWin = 32 * kPer consecutive nonzeros (lane L holds the kPer
+// contiguous elements kPer*L ...):
+//   (0) column indices and values arrive by 16-B vector loads (evict-first);
+//       the next window's are issued as soon as this window's gathers are;
+//   (1) products v * x[c] (x through the read-only path, L2 resident);
+//   (2) row-start flags from the row pointers (one byte per element, shared);
+//   (3) a segmented inclusive scan of the products: sequential inside a lane,
+//       then a 5-step shuffle scan across lanes; the partial sum of a row that
+//       continues from the previous window ("carry") is added to the first
+//       element. A row's sum is the scan value at its last element;
+//   (4) rows ending in the window run the epilogue, lane j <-> the j-th row
+//       still open (groups of 32), inputs loaded by that lane.
+// Rows cut by range boundaries ("split rows") are finished by the last warp
+// to contribute (Sched comment in device_common.cuh).
+//
+// epilogue_walk<Epi> runs the same walk without the products, so a kernel
+// whose reductions must be bit-identical to an epilogue fused into the SpMV
+// (the block-start primal step K3 vs the primal step fused into K2) sees the
+// same row -> lane sequences.
 #pragma once
 
 #include "device_common.cuh"
-#include "tma.cuh"
 
 namespace rhp {
 
-__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-
-// Epilogue per-row inputs: staged by TMA with the tile (1) or loaded by the
-// row's thread into registers at tile start, overlapping the gather (0).
-#ifndef RHP_EPI_TMA
-#define RHP_EPI_TMA 1
-#endif
-constexpr bool kEpiTma = RHP_EPI_TMA != 0;
-
-// Shared-memory layout of one pipeline stage for an epilogue with NIN
-// per-row input vectors. Offsets keep every TMA destination 16-B aligned;
-// the +2/+8/+4 slack absorbs the 16-B alignment of the copied source ranges.
-template <int NIN>
-struct Stage {
-  static constexpr int kVals = kTileNnz + 2;  // doubles
-  static constexpr int kRp = kTileRows + 4;   // int64
-  static constexpr int kIn = kTileRows + 4;   // doubles per input vector
-  static constexpr int kIdx = kTileNnz + 8;   // int32
-  static constexpr size_t off_vals = 0;
-  static constexpr size_t off_rp = align16(off_vals + 8 * kVals);
-  static constexpr size_t off_in = align16(off_rp + 8 * kRp);
-  static constexpr size_t off_idx = align16(off_in + 8 * size_t(kIn) * NIN);
-  static constexpr size_t bytes = align16(off_idx + 4 * kIdx);
+struct WarpSmem {
+  double val[kWin];          // products, then segmented-scan values
+  unsigned char flag[kWin];  // 1 where a row starts
 };
 
-// Dynamic shared memory of spmv_fused<Epi>: two stages, row sums, barriers.
-template <int NIN>
-__host__ __device__ constexpr size_t spmv_smem_bytes() {
-  return 2 * Stage<NIN>::bytes + 8 * kTileRows + 16;
-}
-
-struct TileDesc {
-  int64_t r0, r1, b, e;
-};
-
-__device__ __forceinline__ TileDesc load_desc(const Sched& s, int64_t t) {
-  return TileDesc{s.tile_row[t], s.tile_row_end[t], s.tile_nz[2 * t], s.tile_nz[2 * t + 1]};
-}
-
-// Thread 0: issue the bulk copies of one stream tile into a stage.
-template <class Epi>
-__device__ __forceinline__ void issue_tile(const Csr& A, const Epi& epi, const TileDesc& d,
-                                           unsigned char* stage, uint64_t* bar) {
-  using L = Stage<Epi::NIN>;
-  const int64_t vb = d.b & ~int64_t(1), ve = (d.e + 1) & ~int64_t(1);
-  const int64_t ib = d.b & ~int64_t(3), ie = (d.e + 3) & ~int64_t(3);
-  const int64_t rb = d.r0 & ~int64_t(1), re = (d.r1 + 2) & ~int64_t(1);  // rp needs r1 inclusive
-  const int64_t xb = d.r0 & ~int64_t(1), xe = (d.r1 + 1) & ~int64_t(1);
-  const uint32_t bv = static_cast<uint32_t>(8 * (ve - vb));
-  const uint32_t bi = static_cast<uint32_t>(4 * (ie - ib));
-  const uint32_t br = static_cast<uint32_t>(8 * (re - rb));
-  const uint32_t bx = kEpiTma ? static_cast<uint32_t>(8 * (xe - xb)) : 0u;
-  mbar_arrive_expect_tx(bar, bv + bi + br + bx * Epi::NIN);
-  if (bv) tma_load_1d(stage + L::off_vals, A.v + vb, bv, bar);
-  if (bi) tma_load_1d(stage + L::off_idx, A.ci + ib, bi, bar);
-  tma_load_1d(stage + L::off_rp, A.rp + rb, br, bar);
-  if constexpr (kEpiTma) {
+// Column indices / values of the kPer nonzeros of one lane starting at
+// element i (a multiple of 4). Reads at most 3 elements past the operator's
+// end (inside the 64-B padding of every device array).
+__device__ __forceinline__ void ld_idx(const int32_t* ci, int64_t i, int (&c)[kPer]) {
 #pragma unroll
-    for (int k = 0; k < Epi::NIN; ++k)
-      tma_load_1d(stage + L::off_in + 8 * size_t(L::kIn) * k, epi.in[k] + xb, bx, bar);
+  for (int h = 0; h < kPer / 4; ++h) {
+    const int4 q = __ldcs(reinterpret_cast<const int4*>(ci + i) + h);
+    c[4 * h + 0] = q.x;
+    c[4 * h + 1] = q.y;
+    c[4 * h + 2] = q.z;
+    c[4 * h + 3] = q.w;
   }
 }
 
-template <int W>
-__device__ __forceinline__ void stage_row_sums(const int64_t* rps, int rows, int64_t b,
-                                               const double* prod, double* rowsum) {
-  const int g = threadIdx.x / W, lane = threadIdx.x % W;
-  constexpr int G = kBlock / W;
-  for (int rr = 0; rr < rows; rr += G) {  // uniform trip count: all lanes shuffle
-    const int r = rr + g;
-    double s = 0.0;
-    if (r < rows) {
-      const int lo = static_cast<int>(rps[r] - b), hi = static_cast<int>(rps[r + 1] - b);
-      for (int k = lo + lane; k < hi; k += W) s += prod[k];
-    }
+__device__ __forceinline__ void ld_vals(const double* v, int64_t i, double (&x)[kPer]) {
 #pragma unroll
-    for (int off = W / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0 && r < rows) rowsum[r] = s;
-  }
-}
-
-// Lanes per row group for the shared-memory row sums of a stream tile.
-__device__ __forceinline__ int group_width(int nnz, int rows) {
-  const int mean = rows > 0 ? (nnz + rows - 1) / rows : 1;
-  if (mean <= 4) return 1;
-  if (mean <= 8) return 2;
-  if (mean <= 16) return 4;
-  if (mean <= 32) return 8;
-  if (mean <= 64) return 16;
-  return 32;
-}
-
-template <class Epi>
-__device__ __forceinline__ void compute_tile(const double* __restrict__ xg, const TileDesc& d,
-                                             unsigned char* stage, Epi& epi,
-                                             double (&acc)[Epi::NRED], double* rowsum) {
-  using L = Stage<Epi::NIN>;
-  const int rows = static_cast<int>(d.r1 - d.r0);
-  const int nnz = static_cast<int>(d.e - d.b);
-  double* vals = reinterpret_cast<double*>(stage + L::off_vals) + (d.b & 1);
-  const int* idx = reinterpret_cast<const int*>(stage + L::off_idx) + (d.b & 3);
-  const int64_t* rps = reinterpret_cast<const int64_t*>(stage + L::off_rp) + (d.r0 & 1);
-  const double* ein = reinterpret_cast<const double*>(stage + L::off_in) + (d.r0 & 1);
-  // register path: the row's epilogue inputs, loaded now, used in (3)
-  constexpr int NI = Epi::NIN > 0 ? Epi::NIN : 1;
-  double ereg[NI];
-  if constexpr (!kEpiTma) {
-    if (threadIdx.x < rows) {
-#pragma unroll
-      for (int k = 0; k < Epi::NIN; ++k) ereg[k] = epi.in[k][d.r0 + threadIdx.x];
-    }
-  }
-  // (1) products in place. All indices and all x gathers of a thread are
-  // loaded into registers before the first shared-memory store, so the
-  // kTileNnz/kBlock gathers are in flight together (an interleaved
-  // load/store loop would serialise them on possible aliasing).
-  {
-    constexpr int P = kTileNnz / kBlock;
-    int c[P];
-    double xv[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int i = k * kBlock + threadIdx.x;
-      c[k] = i < nnz ? idx[i] : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < P; ++k) xv[k] = ld_gather(xg + c[k]);
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int i = k * kBlock + threadIdx.x;
-      if (i < nnz) vals[i] = vals[i] * xv[k];
-    }
-  }
-  __syncthreads();
-  // (2) deterministic row sums
-  switch (group_width(nnz, rows)) {
-    case 1: stage_row_sums<1>(rps, rows, d.b, vals, rowsum); break;
-    case 2: stage_row_sums<2>(rps, rows, d.b, vals, rowsum); break;
-    case 4: stage_row_sums<4>(rps, rows, d.b, vals, rowsum); break;
-    case 8: stage_row_sums<8>(rps, rows, d.b, vals, rowsum); break;
-    case 16: stage_row_sums<16>(rps, rows, d.b, vals, rowsum); break;
-    default: stage_row_sums<32>(rps, rows, d.b, vals, rowsum); break;
-  }
-  __syncthreads();
-  // (3) epilogue, thread per row
-  if (threadIdx.x < rows) {
-    if constexpr (kEpiTma)
-      epi.row(d.r0 + threadIdx.x, rowsum[threadIdx.x], ein + threadIdx.x, L::kIn, acc);
-    else
-      epi.row(d.r0 + threadIdx.x, rowsum[threadIdx.x], ereg, 1, acc);
+  for (int h = 0; h < kPer / 2; ++h) {
+    const double2 d = __ldcs(reinterpret_cast<const double2*>(v + i) + h);
+    x[2 * h + 0] = d.x;
+    x[2 * h + 1] = d.y;
   }
 }
 
 template <class Epi>
-__device__ __forceinline__ void tile_chunk(const Csr& A, const double* __restrict__ xg,
-                                           const Sched& s, int64_t chunk, Epi& epi,
-                                           double (&acc)[Epi::NRED]) {
-  __shared__ double red[kWarps];
-  __shared__ double total_s;
-  const int64_t row = s.chunk_row[chunk];
-  const int64_t beg = s.chunk_beg[chunk], end = s.chunk_end[chunk];
-  double s0 = 0.0, s1 = 0.0;
-  int64_t e = beg + threadIdx.x;
-  for (; e + 3 * kBlock < end; e += 4 * kBlock) {
-    const int c0 = ld_stream(A.ci + e), c1 = ld_stream(A.ci + e + kBlock);
-    const int c2 = ld_stream(A.ci + e + 2 * kBlock), c3 = ld_stream(A.ci + e + 3 * kBlock);
-    const double v0 = ld_stream(A.v + e), v1 = ld_stream(A.v + e + kBlock);
-    const double v2 = ld_stream(A.v + e + 2 * kBlock), v3 = ld_stream(A.v + e + 3 * kBlock);
-    s0 = fma(v0, __ldg(xg + c0), s0);
-    s1 = fma(v1, __ldg(xg + c1), s1);
-    s0 = fma(v2, __ldg(xg + c2), s0);
-    s1 = fma(v3, __ldg(xg + c3), s1);
+__device__ __forceinline__ void load_inputs(const Epi& epi, int64_t row,
+                                            double (&ein)[Epi::NIN > 0 ? Epi::NIN : 1]) {
+#pragma unroll
+  for (int k = 0; k < Epi::NIN; ++k) ein[k] = epi.in[k][row];
+}
+
+// Last-arriver completion of a split row: store this warp's partial, and if
+// every contributor has stored, sum them in warp order and run the epilogue
+// (its reductions go to long_red[slot]).
+template <class Epi>
+__device__ __forceinline__ void contribute(const Sched& s, Epi& epi, int slot, int64_t entry,
+                                        double partial) {
+  s.slot_part[entry] = partial;
+  __threadfence();
+  const unsigned int cnt = static_cast<unsigned int>(s.slot_count[slot]);
+  if (atomicAdd(s.slot_ticket + slot, 1u) != cnt - 1) return;
+  __threadfence();
+  const int64_t first = s.slot_first[slot];
+  double t = __ldcg(s.slot_part + 2 * first + 1);  // the first contributor's tail partial
+  for (unsigned int k = 1; k < cnt; ++k) t += __ldcg(s.slot_part + 2 * (first + k));
+  const int64_t row = s.slot_row[slot];
+  double ein[Epi::NIN > 0 ? Epi::NIN : 1];
+  load_inputs(epi, row, ein);
+  double la[Epi::NRED];
+#pragma unroll
+  for (int q = 0; q < Epi::NRED; ++q) la[q] = 0.0;
+  epi.row(row, t, ein, 1, la);
+#pragma unroll
+  for (int q = 0; q < Epi::NRED; ++q) s.long_red[(size_t)slot * 16 + q] = la[q];
+  s.slot_ticket[slot] = 0u;
+}
+
+// One warp's range. WALK: epilogue only (row sums 0), same row -> lane map.
+template <class Epi, bool WALK>
+__device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals,
+                                           const double* __restrict__ xg, const Sched& s,
+                                           Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  if (w >= s.n_warps) return;
+  const int64_t* rp = s.rp;
+  const int64_t row_head = s.warp_row[w], r_end = s.warp_row[w + 1];
+  const int64_t e0 = s.warp_nz[w], e_end = s.warp_nz[w + 1];
+  const int hslot = s.head_slot[w];
+  const int64_t r_lim = r_end < s.rows ? r_end + 1 : s.rows;  // rows whose end may be read
+  int64_t r = row_head;
+  int64_t rstart = rp[r];  // start of row r (warp-uniform)
+  double carry = 0.0;
+  // windows are aligned to 4 nonzeros (16-B vector loads); elements outside
+  // [e0, e_end) are masked to zero
+  int64_t wb = e0 & ~int64_t(3);
+  int cn[kPer];  // column indices of this lane's elements of the current window
+  if constexpr (!WALK) {
+    if (wb + kPer * lane < e_end) ld_idx(ci, wb + kPer * lane, cn);
   }
-  for (; e < end; e += kBlock) s0 = fma(ld_stream(A.v + e), __ldg(xg + ld_stream(A.ci + e)), s0);
-  double v = s0 + s1;
+  for (;; wb += kWin) {
+    const int64_t we = wb + kWin < e_end ? wb + kWin : e_end;  // valid end of the window
+    // ends of the next 32 rows: group 0 of the flags and of the completion pass
+    int64_t re0 = r + lane < r_lim ? rp[r + lane + 1] : INT64_MAX;
+    if constexpr (!WALK) {
+      const int64_t mine = wb + kPer * lane;  // first element of this lane
+      // (1) values and gathers of this window, then the next window's indices
+      double p[kPer], vc[kPer];
+      if (mine < we) ld_vals(vals, mine, vc);
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) t += red[w];
-    total_s = t;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double ein[Epi::NIN > 0 ? Epi::NIN : 1];
-#pragma unroll
-    for (int k = 0; k < Epi::NIN; ++k) ein[k] = epi.in[k][row];
-    const int slot = s.chunk_slot[chunk];
-    if (slot < 0) {
-      epi.row(row, total_s, ein, 1, acc);
-    } else {
-      s.chunk_part[chunk] = total_s;
-      __threadfence();
-      const unsigned int cnt = (unsigned int)s.chunk_count[chunk];
-      if (atomicAdd(s.slot_ticket + slot, 1u) == cnt - 1) {
-        __threadfence();
-        const int first = s.chunk_first[chunk];
-        double t = 0.0;
-        for (unsigned int c = 0; c < cnt; ++c) t += __ldcg(s.chunk_part + first + c);
-        double la[Epi::NRED];
-#pragma unroll
-        for (int q = 0; q < Epi::NRED; ++q) la[q] = 0.0;
-        epi.row(row, t, ein, 1, la);
-#pragma unroll
-        for (int q = 0; q < Epi::NRED; ++q) s.long_red[(size_t)slot * 16 + q] = la[q];
-        s.slot_ticket[slot] = 0u;
+      for (int t = 0; t < kPer; ++t) {
+        const bool ok = mine + t >= e0 && mine + t < we;
+        p[t] = ok ? ld_gather(xg + cn[t]) : 0.0;
+        if (!ok) vc[t] = 0.0;
       }
+      if (mine + kWin < e_end) ld_idx(ci, mine + kWin, cn);
+      // (2) row-start flags
+#pragma unroll
+      for (int h = 0; h < kPer / 4; ++h) reinterpret_cast<uint32_t*>(sm.flag)[lane * (kPer / 4) + h] = 0u;
+      __syncwarp();
+      if (lane == 0 && rstart >= wb && rstart < we) sm.flag[rstart - wb] = 1;
+      for (int64_t g = r, re = re0;;) {
+        if (re >= wb && re < we) sm.flag[re - wb] = 1;
+        if (__shfl_sync(0xffffffffu, re, 31) >= we) break;
+        g += 32;
+        re = g + lane < r_lim ? rp[g + lane + 1] : INT64_MAX;
+      }
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) p[t] = mul(vc[t], p[t]);
+      __syncwarp();
+      // (3) segmented scan
+      uint32_t fl[kPer / 4];
+#pragma unroll
+      for (int h = 0; h < kPer / 4; ++h)
+        fl[h] = reinterpret_cast<const uint32_t*>(sm.flag)[lane * (kPer / 4) + h];
+      auto flag_at = [&](int t) { return (fl[t >> 2] >> (8 * (t & 3))) & 1u; };
+      if (lane == 0 && !flag_at(0)) p[0] = add(carry, p[0]);
+      int hs = 0;
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        if (flag_at(t)) hs = 1;
+        else if (t > 0) p[t] = add(p[t - 1], p[t]);
+      }
+      double agg = p[kPer - 1];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(0xffffffffu, agg, d);
+        const int oh = __shfl_up_sync(0xffffffffu, hs, d);
+        if (lane >= d) {
+          if (!hs) agg = add(o, agg);
+          hs |= oh;
+        }
+      }
+      const double excl = __shfl_up_sync(0xffffffffu, agg, 1);
+      if (lane > 0) {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+          if (flag_at(t)) break;
+          p[t] = add(excl, p[t]);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < kPer / 2; ++h)
+        reinterpret_cast<double2*>(sm.val)[lane * (kPer / 2) + h] = make_double2(p[2 * h], p[2 * h + 1]);
+      __syncwarp();
+    }
+    // (4) rows ending in this window
+    for (int64_t re = re0;;) {
+      const int64_t row = r + lane;
+      const bool inr = row < r_end;
+      if (!inr) re = INT64_MAX;
+      int64_t rs = __shfl_up_sync(0xffffffffu, re, 1);
+      if (lane == 0) rs = rstart;
+      const bool done = inr && re <= we;
+      if (done) {
+        double sum = 0.0;
+        if constexpr (!WALK) sum = re > rs ? sm.val[re - 1 - wb] : 0.0;
+        double ein[Epi::NIN > 0 ? Epi::NIN : 1];
+        if (row == row_head && hslot >= 0) {
+          if constexpr (WALK) {
+            load_inputs(epi, row, ein);
+            double la[Epi::NRED];
+#pragma unroll
+            for (int q = 0; q < Epi::NRED; ++q) la[q] = 0.0;
+            epi.row(row, 0.0, ein, 1, la);
+#pragma unroll
+            for (int q = 0; q < Epi::NRED; ++q) s.long_red[(size_t)hslot * 16 + q] = la[q];
+          } else {
+            contribute(s, epi, hslot, 2 * w, sum);
+          }
+        } else {
+          load_inputs(epi, row, ein);
+          epi.row(row, sum, ein, 1, acc);
+        }
+      }
+      const int nc = __popc(__ballot_sync(0xffffffffu, done));
+      if (nc > 0) rstart = __shfl_sync(0xffffffffu, re, nc - 1);  // end of the last finished row
+      r += nc;
+      if (nc < 32) break;
+      re = r + lane < r_end ? rp[r + lane + 1] : INT64_MAX;
+    }
+    if constexpr (!WALK) {
+      // partial sum of the row left open at the window's end
+      if (we > wb) carry = rstart < we ? sm.val[we - 1 - wb] : 0.0;
+      __syncwarp();  // the next window overwrites the shared arrays
+    }
+    if (wb + kWin >= e_end) break;
+  }
+  if constexpr (!WALK) {
+    // the range ends inside row r_end: contribute its partial
+    if (lane == 0 && r_end < s.rows && e_end > rstart) {
+      if (r_end == row_head && hslot >= 0) contribute(s, epi, hslot, 2 * w, carry);
+      else contribute(s, epi, s.tail_slot[w], 2 * w + 1, carry);
     }
   }
-  __syncthreads();
 }
 
-// Epi provides: NRED (>= 1) reductions, NIN per-row input vectors `in[NIN]`
-// (TMA-staged), REDUCE, FINAL; bool enter() (block-uniform early exit);
-// void row(int64_t i, double rowsum, const double* e, int stride,
-// double(&acc)[NRED]) with input k of row i at e[k*stride]; and, when FINAL,
-// void finalize(const Sched&, const double* part, int grid) (last block).
+// Epi provides: NRED (>= 1) reductions, NIN per-row input vectors `in[NIN]`,
+// REDUCE, FINAL; bool enter() (block-uniform early exit); void row(int64_t
+// i, double rowsum, const double* e, int stride, double(&acc)[NRED]) with
+// input k of row i at e[k*stride]; and, when FINAL, void finalize(const
+// Sched&, const double* part, int grid) (last block).
 template <class Epi>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const double* __restrict__ xg,
                                                                  Sched s, Epi epi, double* part,
                                                                  unsigned int* ticket) {
   if (!epi.enter()) return;
-  extern __shared__ __align__(128) unsigned char smem[];
-  using L = Stage<Epi::NIN>;
-  double* rowsum = reinterpret_cast<double*>(smem + 2 * L::bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * L::bytes + 8 * kTileRows);
+  __shared__ __align__(16) WarpSmem wsm[kWarps];
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  __shared__ TileDesc sdesc[2];  // descriptor of the tile in each stage
-  const int64_t grid = gridDim.x;
-  // Tile order: the chunk tiles of long rows first (longest work first, so
-  // they do not form a tail), then the stream tiles. CTA b takes tiles
-  // b, b+grid, ...; t below indexes stream tiles only.
-  const int64_t n_chunks = s.total_tiles - s.n_stream;
-  int64_t tc = blockIdx.x;
-  int64_t t = tc;
-  if (t < n_chunks) t += ((n_chunks - t + grid - 1) / grid) * grid;
-  t -= n_chunks;
-  TileDesc next{}, after{};
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    if (t < s.n_stream) {  // the first stream tile streams in while chunks run
-      sdesc[0] = load_desc(s, t);
-      issue_tile(A, epi, sdesc[0], smem, &bars[0]);
-    }
-    if (t + grid < s.n_stream) next = load_desc(s, t + grid);
-    if (t + 2 * grid < s.n_stream) after = load_desc(s, t + 2 * grid);
-  }
-  __syncthreads();
-  for (; tc < n_chunks; tc += grid) tile_chunk(A, xg, s, tc, epi, acc);
-  for (int it = 0; t < s.n_stream; t += grid, ++it) {
-    const int st = it & 1;
-    if (threadIdx.x == 0) {
-      if (t + grid < s.n_stream) {
-        fence_proxy_async();  // this stage's previous generic accesses precede the copy
-        sdesc[st ^ 1] = next;
-        issue_tile(A, epi, next, smem + (st ^ 1) * L::bytes, &bars[st ^ 1]);
-      }
-      next = after;
-      if (t + 3 * grid < s.n_stream) after = load_desc(s, t + 3 * grid);
-    }
-    const TileDesc d = sdesc[st];  // written before the barrier ending the previous tile
-    mbar_wait(&bars[st], (it >> 1) & 1);
-    compute_tile(xg, d, smem + st * L::bytes, epi, acc, rowsum);
-    __syncthreads();  // stage st is free for the copy issued next iteration
-  }
+  warp_range<Epi, false>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
   if constexpr (Epi::REDUCE) {
     block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
     if constexpr (Epi::FINAL) {
@@ -319,46 +266,16 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   }
 }
 
-// Runs only the epilogue of spmv_fused<Epi>, with exactly its tile -> block
-// and row -> thread assignment (row sum argument 0, inputs read from global
-// memory). A kernel whose reductions must be bit-identical to the epilogue
-// fused into an SpMV (the block-start primal step vs the primal step fused
-// into the A^T pass) uses this walker so the per-thread accumulation
-// sequences are the same.
+// Runs only the epilogue of spmv_fused<Epi>, with exactly its row -> lane
+// assignment (row sum argument 0, inputs read from global memory).
 template <class Epi>
 __global__ void __launch_bounds__(kBlock) epilogue_walk(Sched s, Epi epi, double* part) {
   if (!epi.enter()) return;
+  __shared__ __align__(16) WarpSmem wsm[kWarps];
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  double ein[Epi::NIN > 0 ? Epi::NIN : 1];
-  const int64_t n_chunks = s.total_tiles - s.n_stream;  // same order as spmv_fused
-  for (int64_t tile = blockIdx.x; tile < s.total_tiles; tile += gridDim.x) {
-    int64_t row = -1;
-    int slot = -1;
-    if (tile >= n_chunks) {
-      const int64_t ts = tile - n_chunks;
-      const int64_t r0 = s.tile_row[ts], r1 = s.tile_row_end[ts];
-      if (r0 + threadIdx.x < r1) row = r0 + threadIdx.x;
-    } else if (threadIdx.x == 0) {
-      const int64_t chunk = tile;
-      slot = s.chunk_slot[chunk];
-      if (slot < 0 || chunk == s.chunk_first[chunk]) row = s.chunk_row[chunk];
-    }
-    if (row < 0) continue;
-#pragma unroll
-    for (int k = 0; k < Epi::NIN; ++k) ein[k] = epi.in[k][row];
-    if (slot < 0) {
-      epi.row(row, 0.0, ein, 1, acc);
-    } else {
-      double la[Epi::NRED];
-#pragma unroll
-      for (int q = 0; q < Epi::NRED; ++q) la[q] = 0.0;
-      epi.row(row, 0.0, ein, 1, la);
-#pragma unroll
-      for (int q = 0; q < Epi::NRED; ++q) s.long_red[(size_t)slot * 16 + q] = la[q];
-    }
-  }
+  warp_range<Epi, true>(nullptr, nullptr, nullptr, s, epi, acc, wsm[threadIdx.x >> 5]);
   block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
   epi.walk_done();
 }

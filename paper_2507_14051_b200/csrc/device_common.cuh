@@ -159,20 +159,60 @@ __device__ __forceinline__ void block_reduce_store(const double (&acc)[N], doubl
   __syncthreads();
 }
 
-// Block-wide fixed-order sum of `count` partials per quantity (SoA, stride);
-// every thread receives the totals.
+// Thread-strided sums of `count` partials per quantity (SoA, `stride`),
+// added into v in index order. The loads of a batch (B per quantity) are all
+// issued before any add, so the finalizing block pays one L2 round trip per
+// batch rather than one per partial — this sum sits on the serial tail of
+// every finalizing kernel.
+template <int N, int B = 2>
+__device__ __forceinline__ void thread_partials(const double* part, int count, int stride,
+                                                double (&v)[N]) {
+  for (int base = 0; base < count; base += B * kBlock) {
+    double t[N][B];
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int i = base + b * kBlock + threadIdx.x;
+        t[q][b] = i < count ? __ldcg(part + (size_t)q * stride + i) : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[q] += t[q][b];
+  }
+}
+
+// The same for the epilogue reductions of split rows (slot-major, 16 apart).
+template <int N, int B = 4>
+__device__ __forceinline__ void thread_slots(const double* long_red, int n_multi, double (&v)[N]) {
+  for (int base = 0; base < n_multi; base += B * kBlock) {
+    double t[N][B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int i = base + b * kBlock + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < N; ++q) t[q][b] = i < n_multi ? __ldcg(long_red + (size_t)i * 16 + q) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[q] += t[q][b];
+  }
+}
+
+// Fixed block tree (xor butterfly, then warps in order) of N per-thread
+// values; every thread receives the totals.
 template <int N>
-__device__ __forceinline__ void block_sum_partials(const double* part, int count, int stride,
-                                                   double (&out)[N]) {
+__device__ __forceinline__ void block_tree(const double (&v)[N], double (&out)[N]) {
   __shared__ double sm[N][kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < N; ++q) {
-    double v = 0.0;
-    for (int i = threadIdx.x; i < count; i += kBlock) v += __ldcg(part + (size_t)q * stride + i);
+    double t = v[q];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) sm[q][warp] = v;
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0) sm[q][warp] = t;
   }
   __syncthreads();
 #pragma unroll
@@ -185,35 +225,65 @@ __device__ __forceinline__ void block_sum_partials(const double* part, int count
   __syncthreads();
 }
 
+// Block-wide fixed-order sum of `count` partials per quantity (SoA, stride);
+// every thread receives the totals.
+template <int N>
+__device__ __forceinline__ void block_sum_partials(const double* part, int count, int stride,
+                                                   double (&out)[N]) {
+  double v[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = 0.0;
+  thread_partials<N>(part, count, stride, v);
+  block_tree<N>(v, out);
+}
+
 // Adds the epilogue reductions of split rows: block-parallel, fixed order
-// (thread-strided sums, then the fixed block tree of block_sum_partials).
+// (thread-strided sums, then the fixed block tree).
 template <int N>
 __device__ __forceinline__ void add_slots(const double* long_red, int n_multi, double (&out)[N]) {
   if (n_multi == 0) return;
-  __shared__ double sm[N][kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v[N], t[N];
 #pragma unroll
-  for (int q = 0; q < N; ++q) {
-    double v = 0.0;
-    for (int i = threadIdx.x; i < n_multi; i += kBlock) v += __ldcg(long_red + (size_t)i * 16 + q);
+  for (int q = 0; q < N; ++q) v[q] = 0.0;
+  thread_slots<N>(long_red, n_multi, v);
+  block_tree<N>(v, t);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) sm[q][warp] = v;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += sm[q][w];
-    out[q] += s;
-  }
-  __syncthreads();
+  for (int q = 0; q < N; ++q) out[q] += t[q];
 }
 
 template <int N>
 __device__ __forceinline__ void add_long_slots(const Sched& s, double (&out)[N]) {
   add_slots<N>(s.long_red, s.n_multi, out);
+}
+
+// The end-of-iteration sums of K1's finalize in one pass: y-side sums t1
+// (K1's partials + A's split-row slots) and x-side sums t3 (the previous
+// primal walker's partials + A^T's split-row slots). All loads are issued
+// before the single block tree. Same values as block_sum_partials followed
+// by add_slots for each side.
+template <int N1, int N3>
+__device__ __forceinline__ void iteration_sums(const double* part1, int grid1, const double* red1,
+                                               int multi1, const double* part3, int grid3,
+                                               const double* red3, int multi3, double (&t1)[N1],
+                                               double (&t3)[N3]) {
+  constexpr int N = 2 * (N1 + N3);
+  double v[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = 0.0;
+  double* a1 = v;
+  double* s1 = v + N1;
+  double* a3 = v + 2 * N1;
+  double* s3 = v + 2 * N1 + N3;
+  thread_partials<N1>(part1, grid1, grid1, *reinterpret_cast<double(*)[N1]>(a1));
+  thread_partials<N3>(part3, grid3, grid3, *reinterpret_cast<double(*)[N3]>(a3));
+  thread_slots<N1>(red1, multi1, *reinterpret_cast<double(*)[N1]>(s1));
+  thread_slots<N3>(red3, multi3, *reinterpret_cast<double(*)[N3]>(s3));
+  double o[N];
+  block_tree<N>(v, o);
+#pragma unroll
+  for (int q = 0; q < N1; ++q) t1[q] = multi1 ? o[q] + o[N1 + q] : o[q];
+#pragma unroll
+  for (int q = 0; q < N3; ++q) t3[q] = multi3 ? o[2 * N1 + q] + o[2 * N1 + N3 + q] : o[2 * N1 + q];
 }
 
 // Last-block-done election. Returns true in exactly one block, after every

@@ -213,10 +213,8 @@ struct EpiDual {
   // Last block: fixed-point residual, restart verdict, counters, stop flag.
   __device__ void finalize(const Sched& s, const double* part, int grid) {
     double t1[5], t3[4];
-    block_sum_partials<5>(part, grid, grid, t1);
-    add_long_slots<5>(s, t1);
-    block_sum_partials<4>(part3, grid3, grid3, t3);
-    add_slots<4>(long_red3, n_multi3, t3);
+    iteration_sums<5, 4>(part, grid, s.long_red, s.n_multi, part3, grid3, long_red3, n_multi3, t1,
+                         t3);
     if (threadIdx.x != 0) return;
     if (xchg) {  // row-partitioned: publish the local y-side sums, control after the allreduce
 #pragma unroll

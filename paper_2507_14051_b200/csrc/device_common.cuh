@@ -61,18 +61,23 @@ __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((
 
 // Random gather of the SpMV input vector (L2 resident, almost never an L1 hit).
 #ifndef RHP_GATHER_MODE
-#define RHP_GATHER_MODE 0
+#define RHP_GATHER_MODE 2
 #endif
 __device__ __forceinline__ double ld_gather(const double* p) {
 #if RHP_GATHER_MODE == 1
   return __ldcg(p);  // L2 only
 #elif RHP_GATHER_MODE == 2
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 #else
   return __ldg(p);  // read-only path
 #endif
+}
+
+// Bulk L2 prefetch (address and size multiples of 16 B; no completion).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // Loop control shared by host and device (one per ctx, device resident).

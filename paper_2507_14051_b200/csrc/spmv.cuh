@@ -39,6 +39,14 @@
 
 namespace rhp {
 
+// Slot of window element e in WarpSmem::val: element t of lane L at
+// t * 32 + L, so the scan-value stores of a warp (one per t) hit 32
+// consecutive doubles (2 wavefronts, no bank conflicts).
+__device__ __forceinline__ int sv(int64_t e) {
+  const unsigned u = static_cast<unsigned>(e);  // 0 <= e < kWin
+  return static_cast<int>((u % kPer) * 32u + u / kPer);
+}
+
 struct WarpSmem {
   double val[kWin];          // products, then segmented-scan values
   unsigned char flag[kWin];  // 1 where a row starts
@@ -135,7 +143,11 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
 #pragma unroll
       for (int t = 0; t < kPer; ++t) {
         const bool ok = mine + t >= e0 && mine + t < we;
+#ifdef RHP_FAKE_GATHER  // timing experiment only: gathers confined to 32 KB of x (L1 hits)
+        p[t] = ok ? ld_gather(xg + (cn[t] & 0xfff)) : 0.0;
+#else
         p[t] = ok ? ld_gather(xg + cn[t]) : 0.0;
+#endif
         if (!ok) vc[t] = 0.0;
       }
       if (mine + kWin < e_end) ld_idx(ci, mine + kWin, cn);
@@ -185,8 +197,7 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
         }
       }
 #pragma unroll
-      for (int h = 0; h < kPer / 2; ++h)
-        reinterpret_cast<double2*>(sm.val)[lane * (kPer / 2) + h] = make_double2(p[2 * h], p[2 * h + 1]);
+      for (int t = 0; t < kPer; ++t) sm.val[sv(kPer * lane + t)] = p[t];
       __syncwarp();
     }
     // (4) rows ending in this window
@@ -199,7 +210,7 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
       const bool done = inr && re <= we;
       if (done) {
         double sum = 0.0;
-        if constexpr (!WALK) sum = re > rs ? sm.val[re - 1 - wb] : 0.0;
+        if constexpr (!WALK) sum = re > rs ? sm.val[sv(re - 1 - wb)] : 0.0;
         double ein[Epi::NIN > 0 ? Epi::NIN : 1];
         if (row == row_head && hslot >= 0) {
           if constexpr (WALK) {
@@ -226,7 +237,7 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
     }
     if constexpr (!WALK) {
       // partial sum of the row left open at the window's end
-      if (we > wb) carry = rstart < we ? sm.val[we - 1 - wb] : 0.0;
+      if (we > wb) carry = rstart < we ? sm.val[sv(we - 1 - wb)] : 0.0;
       __syncwarp();  // the next window overwrites the shared arrays
     }
     if (wb + kWin >= e_end) break;

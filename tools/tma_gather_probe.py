@@ -6,7 +6,9 @@ Every variant computes sum(v[i] * x[idx[i]]) over C2's own column indices
 (10M random gathers into an 8 MB, L2-resident x) and is timed with CUDA
 events:
 
-  ldg      — LDG gathers, 8 per thread in flight (the SpMV engine's path)
+  ldg      — LDG gathers, U per thread in flight (the SpMV engine's path)
+  ldgsts   — cp.async 8-B gathers straight into shared memory (no registers
+             held while in flight), 2-stage ring per warp
   g4w4     — TMA tile::gather4 over x viewed as [n/4, 4] (32-B rows = one L2
              sector per gather), each lane issues one gather4 per 128-nnz chunk
   g4w2     — the same over x viewed as [n/2, 2] (16-B rows)
@@ -126,6 +128,41 @@ __global__ void __launch_bounds__(128) k_tma(const int* __restrict__ idx, const 
   out[(long)blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// cp.async (LDGSTS) gathers: each warp owns a 2-stage ring of 2 x 256
+// doubles; lane L gathers elements L + 32 t of a 256-element chunk.
+template <int NS>
+__global__ void __launch_bounds__(256) k_ldgsts(const int* __restrict__ idx, const double* __restrict__ v,
+                                                const double* __restrict__ x, long nchunks, double* out) {
+  __shared__ __align__(16) double ring[8][NS][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long wg = (long)blockIdx.x * 8 + warp, nw = (long)gridDim.x * 8;
+  auto issue = [&](long ch, int s) {
+    if (ch < nchunks) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int c = __ldcs(idx + ch * 256 + t * 32 + lane);
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(&ring[warp][s][t * 32 + lane]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(x + c) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) issue(wg + s * nw, s);
+  int s = 0;
+  for (long ch = wg; ch < nchunks; ch += nw) {
+    issue(ch + (long)(NS - 1) * nw, (s + NS - 1) % NS);
+    asm volatile("cp.async.wait_group %0;" :: "n"(NS - 1) : "memory");
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc = fma(__ldcs(v + ch * 256 + t * 32 + lane), ring[warp][s][t * 32 + lane], acc);
+    __syncwarp();
+    s = (s + 1) % NS;
+  }
+  out[(long)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -158,7 +195,17 @@ double run(torch::Tensor idx, torch::Tensor v, torch::Tensor x, torch::Tensor ou
   CUtensorMap m4 = make_map(xp, x.numel(), 4), m2 = make_map(xp, x.numel(), 2);
   auto launch = [&]() {
     const size_t shm = (size_t)4 * nb * 4096;
-    if (variant == 0) { k_ldg<8><<<blocks, 256>>>(ip, vp, xp, nchunks * 128, op); return; }
+    if (variant == 0) {
+      if (nb == 16) k_ldg<16><<<blocks, 256>>>(ip, vp, xp, nchunks * 128, op);
+      else if (nb == 4) k_ldg<4><<<blocks, 256>>>(ip, vp, xp, nchunks * 128, op);
+      else k_ldg<8><<<blocks, 256>>>(ip, vp, xp, nchunks * 128, op);
+      return;
+    }
+    if (variant == 4) {
+      if (nb == 2) k_ldgsts<2><<<blocks, 256>>>(ip, vp, xp, nchunks / 2, op);
+      else k_ldgsts<3><<<blocks, 256>>>(ip, vp, xp, nchunks / 2, op);
+      return;
+    }
 #define L(MODE, NB) { auto k = k_tma<MODE, NB>; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm); \
       k<<<blocks, 128, shm>>>(ip, vp, MODE == 1 ? m2 : m4, xp, nchunks, op); }
     if (nb == 2) { if (variant == 1) L(0, 2) else if (variant == 2) L(1, 2) else L(2, 2) }
@@ -182,12 +229,13 @@ double run(torch::Tensor idx, torch::Tensor v, torch::Tensor x, torch::Tensor ou
 """
 CPP_SRC = ("double run(torch::Tensor idx, torch::Tensor v, torch::Tensor x, torch::Tensor out, int variant, "
            "int blocks, int nb, int reps);")
-NAMES = {0: "ldg", 1: "g4w4", 2: "g4w2", 3: "bulk16"}
+NAMES = {0: "ldg", 1: "g4w4", 2: "g4w2", 3: "bulk16", 4: "ldgsts"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/tma_gather.json")
+    ap.add_argument("--variants", default="0,1,2,3")
     args = ap.parse_args()
     mod = load_inline("tma_gather_probe", CPP_SRC, cuda_sources=CUDA_SRC, functions=["run"],
                       extra_cuda_cflags=["-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo"],
@@ -200,10 +248,14 @@ def main():
     x = torch.randn(lp.num_vars + 8, dtype=torch.float64, device="cuda")
     ref = float((v.cpu() * x.cpu()[idx.cpu().long()]).sum())
     res = []
-    for variant in (0, 1, 2, 3):
-        for per_sm in ((3, 4, 6) if variant == 0 else (2, 3, 4, 6)):
-            for nb in ((0,) if variant == 0 else (2, 4, 8)):
-                if variant and per_sm * 4 * nb * 4096 > 220 * 1024:
+    grid = {0: ((2, 3, 4, 6), (4, 8, 16)), 1: ((2, 3, 4, 6), (2, 4, 8)), 2: ((2, 3, 4, 6), (2, 4, 8)),
+            3: ((2, 3, 4, 6), (2, 4, 8)), 4: ((1, 2, 3, 4), (2, 3))}
+    for variant in [int(v) for v in args.variants.split(",")]:
+        for per_sm in grid[variant][0]:
+            for nb in grid[variant][1]:
+                if variant in (1, 2, 3) and per_sm * 4 * nb * 4096 > 220 * 1024:
+                    continue
+                if variant == 4 and per_sm * 8 * nb * 2048 > 220 * 1024:
                     continue
                 blocks = sms * per_sm
                 out = torch.zeros(blocks * 256, dtype=torch.float64, device="cuda")

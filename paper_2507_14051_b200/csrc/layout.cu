@@ -7,12 +7,22 @@
 
 #include "layout.cuh"
 
+#ifndef RHP_SNAP_WINS
+#define RHP_SNAP_WINS 8
+#endif
+#ifndef RHP_SNAP_FRAC
+#define RHP_SNAP_FRAC 1.25
+#endif
+
 namespace rhp {
 
 // Merge-path warp ranges (Sched in device_common.cuh). Boundary k sits at
 // cost k * total / W, cost(r, e) = e + row_weight * r; it snaps to the nearer
-// row start unless the row is longer than the snap length, in which case the
-// row is split there. Consecutive boundaries inside one row share its slot.
+// row start unless the row is longer than the snap length (min(8 windows,
+// 1.25 ranges): a warp may take up to 1.25x its share rather than split a row
+// — split rows cost a fence, a ticket and a serial sum at the range end; C3's
+// 1000-nonzero rows: K1 33 -> 23 us), in which case the row is split there.
+// Consecutive boundaries inside one row share its slot.
 void build_schedule(HostOperator& op, int64_t n_warps, double row_weight) {
   const int64_t W = std::max<int64_t>(1, n_warps);
   const int64_t R = op.rows, Z = op.nnz;
@@ -25,7 +35,8 @@ void build_schedule(HostOperator& op, int64_t n_warps, double row_weight) {
   op.warp_nz[0] = 0;
   const double total = static_cast<double>(Z) + row_weight * static_cast<double>(R);
   const double per = total / static_cast<double>(W);
-  const int64_t snap = std::max<int64_t>(1, std::min<int64_t>(2 * kWin, static_cast<int64_t>(per / 2)));
+  const int64_t snap = std::max<int64_t>(
+      1, std::min<int64_t>(RHP_SNAP_WINS * kWin, static_cast<int64_t>(per * RHP_SNAP_FRAC)));
   auto cost = [&](int64_t r) { return static_cast<double>(rp[r]) + row_weight * static_cast<double>(r); };
   int64_t pr = 0, pe = 0;
   for (int64_t k = 1; k < W; ++k) {

@@ -10,8 +10,10 @@
 // Each operator gets a merge-path warp schedule (spmv.cuh) once the grid is
 // known (build_schedule).
 //
-// The permutation maps (prow/pcol) are kept in the interface for layouts
-// that reorder rows; the current layout is the identity.
+// The operators are built on the device (ingest.cu); the host keeps the row
+// pointers for the schedules. The permutation maps (prow/pcol) are kept in
+// the interface for layouts that reorder rows; the current layout is the
+// identity.
 #pragma once
 
 #include <cstdint>
@@ -35,11 +37,11 @@ inline int row_kind(int64_t L) {
   return 7;
 }
 
+// Host side of a device operator: its row pointers (the column indices and
+// values live on the device only, ingest.cu) and its warp schedule.
 struct HostOperator {
   int64_t rows = 0, cols = 0, nnz = 0;
   std::vector<int64_t> rp;
-  std::vector<int32_t> ci;
-  std::vector<double> v;
   Sched sched{};  // host copy; device pointers filled at upload
   // warp schedule (Sched in device_common.cuh)
   std::vector<int64_t> warp_row, warp_nz, slot_row;
@@ -54,16 +56,8 @@ struct HostLayout {
   int64_t nnz = 0;                     // local nonzeros (explicit zeros dropped)
   std::vector<int32_t> prow;           // device row -> original row (global index)
   std::vector<int32_t> pcol;           // device col -> original col
-  std::vector<int32_t> icol;           // original col -> device col
-  std::vector<int64_t> a_dev_to_csr;   // device A element -> reference CSR position (local)
-  std::vector<int64_t> at_dev_to_csc;  // device A^T element -> reference CSC position (local)
   HostOperator A, At;
 };
-
-// Builds the layout of rows [row_begin, row_end) of the LP. Throws
-// std::out_of_range (bad index), std::domain_error (non-finite value,
-// duplicate/unsorted entry), std::invalid_argument (too large).
-void build_layout(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end, HostLayout& out);
 
 // Merge-path warp schedule of one operator for n_warps warps: ranges
 // balanced by nonzeros + row_weight * rows, boundaries snapped to row starts

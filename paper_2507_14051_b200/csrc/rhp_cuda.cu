@@ -19,6 +19,7 @@
 #include <nccl.h>
 #endif
 
+#include "ingest.cuh"
 #include "layout.cuh"
 #include "pdhg_kernels.cuh"
 #include "resident.cuh"
@@ -31,9 +32,7 @@ namespace {
 
 thread_local std::string g_err;
 
-struct CudaError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
+using CudaError = rhp::DeviceFailure;
 
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -64,19 +63,10 @@ int guarded(F&& f) {
   }
 }
 
-// Every device array gets 64 B of zeroed tail padding: the SpMV's bulk copies
-// round source ranges out to 16-B boundaries and may read past the last
-// element (never used).
+// Every device array gets 64 B of zeroed tail padding (ingest.cuh).
 template <class T>
 T* dev_alloc(size_t count) {
-  void* p = nullptr;
-  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 64;
-  CK(cudaMalloc(&p, bytes));
-  // synchronous: the ctx stream is non-blocking, so an asynchronous memset on
-  // the legacy stream could land after later uploads on the ctx stream
-  CK(cudaMemset(p, 0, bytes));
-  CK(cudaDeviceSynchronize());
-  return static_cast<T*>(p);
+  return dev_alloc_zero<T>(count);
 }
 
 template <class T>
@@ -84,13 +74,8 @@ void upload(T* dst, const T* src, size_t count, cudaStream_t s) {
   if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
 }
 
-struct DevOp {
-  int64_t rows = 0, nnz = 0;
-  int64_t* rp = nullptr;
-  int32_t* ci = nullptr;
-  double* v = nullptr;       // current values (original, then scaled)
-  double* v_orig = nullptr;  // original values, kept until scaling is done
-  Sched sched{};             // with device pointers
+struct DevOp : DeviceCsr {
+  Sched sched{};  // with device pointers
   int64_t *warp_row = nullptr, *warp_nz = nullptr, *slot_row = nullptr;
   int32_t *head_slot = nullptr, *tail_slot = nullptr, *slot_first = nullptr, *slot_count = nullptr;
   double *slot_part = nullptr, *long_red = nullptr;
@@ -155,19 +140,6 @@ int occupancy_blocks(const void* fn) {
   int b = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
   return std::max(b, 1);
-}
-
-void upload_op(DevOp& d, const HostOperator& h, cudaStream_t s) {
-  d.rows = h.rows;
-  d.nnz = h.nnz;
-  d.rp = dev_alloc<int64_t>(h.rp.size());
-  d.ci = dev_alloc<int32_t>(h.ci.size());
-  d.v = dev_alloc<double>(h.v.size());
-  d.v_orig = dev_alloc<double>(h.v.size());
-  upload(d.rp, h.rp.data(), h.rp.size(), s);
-  upload(d.ci, h.ci.data(), h.ci.size(), s);
-  upload(d.v, h.v.data(), h.v.size(), s);
-  upload(d.v_orig, h.v.data(), h.v.size(), s);
 }
 
 // Uploads the warp schedule of an operator (built for the operator's grid).
@@ -656,16 +628,14 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       c->offsets = partition_rows(*lp, c->world);
       for (int r = 0; r < c->world; ++r)
         c->max_local = std::max(c->max_local, c->offsets[r + 1] - c->offsets[r]);
-      build_layout(*lp, c->offsets[c->rank], c->offsets[c->rank + 1], c->L);
+      ingest_device(*lp, c->offsets[c->rank], c->offsets[c->rank + 1], c->L, c->A, c->At, c->stream);
     } else {
-      build_layout(*lp, 0, lp->num_cons, c->L);
+      ingest_device(*lp, 0, lp->num_cons, c->L, c->A, c->At, c->stream);
     }
     const HostLayout& L = c->L;
     c->m = L.m;
     c->n = L.n;
     cudaStream_t s = c->stream;
-    upload_op(c->A, L.A, s);
-    upload_op(c->At, L.At, s);
     const size_t m = static_cast<size_t>(c->m), n = static_cast<size_t>(c->n);
     for (double** p2 : {&c->c, &c->vl, &c->vu, &c->co, &c->vlo, &c->vuo, &c->cs, &c->x, &c->aty,
                         &c->x0, &c->aty0, &c->xp, &c->xout, &c->rcout, &c->pv, &c->pw})
@@ -867,19 +837,10 @@ int rhp_get_scaled(rhp_ctx* c, const rhp_scaled_out* o) {
   return guarded([&] {
     const HostLayout& L = c->L;
     const std::vector<int32_t> lrows = local_rows(*c);
-    auto pull = [&](double* dst, const double* src, size_t cnt) {
-      std::vector<double> t(cnt);
-      if (cnt) CK(cudaMemcpy(t.data(), src, cnt * sizeof(double), cudaMemcpyDeviceToHost));
-      return t;
-    };
-    if (o->csr_values) {
-      auto t = pull(nullptr, c->A.v, static_cast<size_t>(L.nnz));
-      for (size_t e = 0; e < t.size(); ++e) o->csr_values[L.a_dev_to_csr[e]] = t[e];
-    }
-    if (o->csc_values) {
-      auto t = pull(nullptr, c->At.v, static_cast<size_t>(L.nnz));
-      for (size_t e = 0; e < t.size(); ++e) o->csc_values[L.at_dev_to_csc[e]] = t[e];
-    }
+    // device element order = the reference's CSR / CSC order
+    const size_t nz = static_cast<size_t>(L.nnz);
+    if (o->csr_values && nz) CK(cudaMemcpy(o->csr_values, c->A.v, nz * sizeof(double), cudaMemcpyDeviceToHost));
+    if (o->csc_values && nz) CK(cudaMemcpy(o->csc_values, c->At.v, nz * sizeof(double), cudaMemcpyDeviceToHost));
     if (o->row_scale) download_perm(o->row_scale, c->rs, lrows, c->hbuf, c->stream);
     if (o->col_scale) download_perm(o->col_scale, c->cs, L.pcol, c->hbuf, c->stream);
     if (o->objective) download_perm(o->objective, c->c, L.pcol, c->hbuf, c->stream);

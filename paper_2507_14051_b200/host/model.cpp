@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <memory>
+#include <mutex>
 #include <string>
 
 #include "device.hpp"
@@ -52,7 +54,6 @@ SparseMatrix::SparseMatrix(Index rows, Index cols, std::vector<Triplet> entries)
     val_csr_.push_back(entries[k].value);
   }
   for (Index i = 0; i < rows; ++i) row_ptr_[i + 1] += row_ptr_[i];
-  build_csc();
 }
 
 SparseMatrix SparseMatrix::from_csr(Index rows, Index cols, std::vector<Index> row_ptr,
@@ -63,9 +64,7 @@ SparseMatrix SparseMatrix::from_csr(Index rows, Index cols, std::vector<Index> r
   SparseMatrix a;
   a.rows_ = rows;
   a.cols_ = cols;
-  a.row_ptr_.assign(static_cast<size_t>(rows) + 1, 0);
-  a.col_idx_.reserve(values.size());
-  a.val_csr_.reserve(values.size());
+  bool zeros = false;
   for (Index i = 0; i < rows; ++i) {
     Index prev = -1;
     if (row_ptr[i + 1] < row_ptr[i]) throw UsageError("from_csr: row_ptr not monotone");
@@ -82,29 +81,49 @@ SparseMatrix SparseMatrix::from_csr(Index rows, Index cols, std::vector<Index> r
         throw InvalidProblemError("duplicate or unsorted matrix entry (" + std::to_string(i) +
                                   "," + std::to_string(j) + ")");
       prev = j;
-      if (v == 0.0) continue;
-      a.col_idx_.push_back(j);
-      a.val_csr_.push_back(v);
+      zeros |= v == 0.0;
+    }
+  }
+  if (row_ptr[0] == 0 && static_cast<size_t>(row_ptr[rows]) == values.size() && !zeros) {
+    a.row_ptr_ = std::move(row_ptr);  // already canonical: take the arrays
+    a.col_idx_ = std::move(col_index);
+    a.val_csr_ = std::move(values);
+    return a;
+  }
+  a.row_ptr_.assign(static_cast<size_t>(rows) + 1, 0);
+  a.col_idx_.reserve(values.size());
+  a.val_csr_.reserve(values.size());
+  for (Index i = 0; i < rows; ++i) {
+    for (Index e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      if (values[e] == 0.0) continue;
+      a.col_idx_.push_back(col_index[e]);
+      a.val_csr_.push_back(values[e]);
     }
     a.row_ptr_[i + 1] = static_cast<Index>(a.col_idx_.size());
   }
-  a.build_csc();
   return a;
 }
 
-void SparseMatrix::build_csc() {
-  col_ptr_.assign(static_cast<size_t>(cols_) + 1, 0);
-  for (Index j : col_idx_) col_ptr_[static_cast<size_t>(j) + 1]++;
-  for (Index j = 0; j < cols_; ++j) col_ptr_[j + 1] += col_ptr_[j];
-  row_idx_.resize(col_idx_.size());
-  val_csc_.resize(col_idx_.size());
-  std::vector<Index> fill(col_ptr_.begin(), col_ptr_.end() - 1);
-  for (Index i = 0; i < rows_; ++i)
-    for (Index e = row_ptr_[i]; e < row_ptr_[i + 1]; ++e) {
-      const Index s = fill[col_idx_[e]]++;
-      row_idx_[s] = i;
-      val_csc_[s] = val_csr_[e];
-    }
+const SparseMatrix::Csc& SparseMatrix::csc() const {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!csc_) {
+    auto c = std::make_shared<Csc>();
+    c->col_ptr.assign(static_cast<size_t>(cols_) + 1, 0);
+    for (Index j : col_idx_) c->col_ptr[static_cast<size_t>(j) + 1]++;
+    for (Index j = 0; j < cols_; ++j) c->col_ptr[j + 1] += c->col_ptr[j];
+    c->row_idx.resize(col_idx_.size());
+    c->val.resize(col_idx_.size());
+    std::vector<Index> fill(c->col_ptr.begin(), c->col_ptr.end() - 1);
+    for (Index i = 0; i < rows_; ++i)
+      for (Index e = row_ptr_[i]; e < row_ptr_[i + 1]; ++e) {
+        const Index s = fill[col_idx_[e]]++;
+        c->row_idx[s] = i;
+        c->val[s] = val_csr_[e];
+      }
+    csc_ = std::move(c);
+  }
+  return *csc_;
 }
 
 namespace {
@@ -166,9 +185,12 @@ SparseMatrix SparseMatrix::scaled(std::span<const double> row_scale,
   for (Index i = 0; i < rows_; ++i)
     for (Index e = row_ptr_[i]; e < row_ptr_[i + 1]; ++e)
       r.val_csr_[e] = row_scale[i] * val_csr_[e] * col_scale[col_idx_[e]];
+  const Csc& c = csc();
+  auto rc = std::make_shared<Csc>(c);
   for (Index j = 0; j < cols_; ++j)
-    for (Index e = col_ptr_[j]; e < col_ptr_[j + 1]; ++e)
-      r.val_csc_[e] = col_scale[j] * val_csc_[e] * row_scale[row_idx_[e]];
+    for (Index e = c.col_ptr[j]; e < c.col_ptr[j + 1]; ++e)
+      rc->val[e] = col_scale[j] * c.val[e] * row_scale[c.row_idx[e]];
+  r.csc_ = std::move(rc);
   return r;
 }
 

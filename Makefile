@@ -20,7 +20,7 @@ all: $(LIB)/librhp_cuda.so $(LIB)/librhpdhg.so oracle
 
 $(LIB)/librhp_cuda.so: $(CU_SRCS) $(CU_HDRS)
 	@mkdir -p $(LIB)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) -lnccl 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) -ldl 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
 $(LIB)/librhpdhg.so: $(HOST_SRCS) $(HOST_HDRS) $(LIB)/librhp_cuda.so
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -lrhp_cuda -lz -Wl,-rpath,'$$ORIGIN'

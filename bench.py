@@ -177,7 +177,11 @@ WORKLOADS = {
     "c2": "C2 synthetic MIPLIB-relaxation-like LP (m=500k, n=1M, ~10M nnz, power-law rows)",
     "c3": "C3 synthetic transportation LP (1k x 1k, n=1M, 2M nnz)",
     "c4": "C4 synthetic multicommodity-flow LP (K=20, E=1M, n=20M, 60M nnz)",
+    "c5": "C5 synthetic row-partitionable LP (m=50M, n=20M, ~1B nnz, power-law rows)",
 }
+# C5's CPU sample: the reference on the same generator at 1/50 scale (20M
+# nonzeros), per-iteration and setup cost extrapolated linearly in nonzeros
+C5_CPU_SAMPLE = dict(m=1_000_000, n=400_000)
 
 
 # --------------------------------------------------------------- CPU arm -----
@@ -315,8 +319,16 @@ def run_product(args):
     dominant = "k2" if kt["k2_aty_spmv_primal_ms"] >= kt["k1_dual_spmv_ms"] else "k1"
     achieved = k2 if dominant == "k2" else k1
     iter_bytes = k1b + k2b
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(args.config)
+        if t and dist.world == 1:
+            traffic = t.get(dominant)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json (ncu dram read+write per launch)"
+                if traffic else None,
                 "kernel": ("spmv_fused<EpiAty> (A^T y+ + aty Halpern + next primal step)"
                            if dominant == "k2" else
                            "spmv_fused<EpiDual> (A x+ + dual step + Halpern/reflection)"),
@@ -360,7 +372,18 @@ def run_product(args):
 
     cpu = None
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
-        cpu = cpu_sample(lp, args.cpu_iters, WORKLOADS[args.config])
+        if args.config == "c5":
+            small = generators.c5_rowpart(**C5_CPU_SAMPLE)
+            cpu = cpu_sample(small, args.cpu_iters, "C5 generator at 1/50 scale")
+            ratio = lp.nnz / small.nnz
+            cpu["value"] /= ratio
+            cpu["setup_seconds"] *= ratio
+            cpu["sample"] = (f"the reference on the C5 generator at m={small.num_cons}, "
+                             f"n={small.num_vars}, {small.nnz} nnz (setup + {args.cpu_iters} "
+                             f"iterations, 1 thread); iter/s and setup extrapolated linearly in "
+                             f"nonzeros (x{ratio:.1f})")
+        else:
+            cpu = cpu_sample(lp, args.cpu_iters, WORKLOADS[args.config])
         if e2e and e2e["status"] == "optimal":
             it = e2e["iterations"]
             cpu["time_to_tol_extrapolated_s"] = cpu["setup_seconds"] + it / cpu["value"]

@@ -17,7 +17,10 @@
 
 namespace rhp {
 
-constexpr int kBlock = 256;          // threads per CTA for every hot kernel
+#ifndef RHP_BLOCK
+#define RHP_BLOCK 256
+#endif
+constexpr int kBlock = RHP_BLOCK;    // threads per CTA for every hot kernel
 constexpr int kWarps = kBlock / 32;
 // SpMV engine (spmv.cuh): every warp owns one contiguous merge-path range of
 // its operator and walks it in windows of kWin = 32 * kPer nonzeros.
@@ -79,6 +82,17 @@ __device__ __forceinline__ double ld_gather(const double* p) {
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+
+// 32-bit row / nonzero positions inside the SpMV warp walk.
+#ifndef RHP_IDX32
+#define RHP_IDX32 1
+#endif
+
+// K1/K2 pairs per body of the block graph's WHILE node.
+#ifndef RHP_GRAPH_UNROLL
+#define RHP_GRAPH_UNROLL 2
+#endif
+constexpr int kGraphUnroll = RHP_GRAPH_UNROLL;
 
 // Loop control shared by host and device (one per ctx, device resident).
 struct Ctl {

@@ -152,7 +152,8 @@ void ingest_device(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end,
   L.m = m;
   const int64_t base = m > 0 ? lp.row_ptr[row_begin] : 0;
   const int64_t z0 = m > 0 ? lp.row_ptr[row_end] - base : 0;
-  if (z0 >= INT32_MAX) throw std::invalid_argument("device layout supports at most 2^31-1 nonzeros per GPU");
+  if (z0 >= INT32_MAX - (1 << 16))  // 32-bit positions in the SpMV walk (spmv.cuh)
+    throw std::invalid_argument("device layout supports at most 2^31 - 2^16 nonzeros per GPU");
   for (int64_t i = row_begin; i < row_end; ++i)
     if (lp.row_ptr[i + 1] < lp.row_ptr[i]) throw std::invalid_argument("row_ptr not monotone");
 

@@ -175,10 +175,11 @@ struct EpiDual {
   const double* long_red3; //   primal partial slots
   double* xchg;            // row-partitioned path: where the y-side sums go (else null)
   int token;               // launch index inside a plain (non-graph) block
+  int guard;               // graph copy > 0 of an unrolled body: skip once stopped
   double sigma, sigma_inv, a, b, g, opg;
 
   __device__ bool enter() {
-    if (!ctl->graph_mode && ctl->stop && !ctl->bench) return false;
+    if ((guard || !ctl->graph_mode) && ctl->stop && !ctl->bench) return false;
     sigma = ctl->sigma;
     sigma_inv = ctl->sigma_inv;
     const int64_t k = ctl->k;
@@ -291,11 +292,12 @@ struct EpiAty {
   PrimalOut o;
   const double* in[NIN];
   int token;
+  int guard;  // graph copy > 0 of an unrolled body: run only after its own K1
   double a, b, a2, b2, g, opg, tau;
   int stop;
 
   __device__ bool enter() {
-    if (!ctl->graph_mode && ctl->k1_token != token && !ctl->bench) return false;
+    if ((guard || !ctl->graph_mode) && ctl->k1_token != token && !ctl->bench) return false;
     const int64_t k = ctl->k;  // already incremented by K1's finalize
     a = halpern_a(k - 1);
     b = halpern_b(k - 1);

@@ -16,6 +16,7 @@
 #include <vector>
 
 #ifdef RHP_WITH_NCCL
+#include <dlfcn.h>
 #include <nccl.h>
 #endif
 
@@ -39,6 +40,38 @@ void check(cudaError_t e, const char* what) {
     throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
 }
 #define CK(call) check((call), #call)
+
+#ifdef RHP_WITH_NCCL
+// NCCL is resolved at run time (dlopen of libnccl.so.2) rather than linked:
+// a single-GPU user never loads it, and in a process where PyTorch already
+// loaded its own NCCL the same library is reused — linking the system copy
+// would shadow torch's newer one and break `import torch` afterwards.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    return a;
+  }();
+  if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllReduce || !api.AllGather)
+    throw rhp::DeviceFailure("NCCL (libnccl.so.2) not found: the row-partitioned path needs it");
+  return api;
+}
+#endif
 
 template <class F>
 int guarded(F&& f) {
@@ -272,7 +305,7 @@ EpiAty epi_aty(rhp_ctx& c, int token) {
 
 void allreduce(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
 #ifdef RHP_WITH_NCCL
-  if (ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c.comm, s) != ncclSuccess)
+  if (nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, c.comm, s) != ncclSuccess)
     throw CudaError("ncclAllReduce failed");
 #else
   (void)c, (void)buf, (void)count, (void)s;
@@ -282,7 +315,7 @@ void allreduce(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
 
 void allreduce_max(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
 #ifdef RHP_WITH_NCCL
-  if (ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, c.comm, s) != ncclSuccess)
+  if (nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, c.comm, s) != ncclSuccess)
     throw CudaError("ncclAllReduce(max) failed");
 #else
   (void)c, (void)buf, (void)count, (void)s;
@@ -290,10 +323,13 @@ void allreduce_max(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
 #endif
 }
 
-void launch_iteration(rhp_ctx& c, int token, cudaStream_t s) {
+void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false) {
   if (!c.dist) {
-    launch_spmv(c, c.A, c.grid_a, c.xp, epi_dual(c, token), c.part1, &c.ctl->ticket_dual, s);
-    launch_spmv(c, c.At, c.grid_at, c.yp, epi_aty(c, token), c.part3, nullptr, s);
+    EpiDual d = epi_dual(c, token);
+    EpiAty a = epi_aty(c, token);
+    d.guard = a.guard = guard ? 1 : 0;
+    launch_spmv(c, c.A, c.grid_a, c.xp, d, c.part1, &c.ctl->ticket_dual, s);
+    launch_spmv(c, c.At, c.grid_at, c.yp, a, c.part3, nullptr, s);
     return;
   }
   // row-partitioned: local A x+ with the dual epilogue (y-side sums -> xchg[n..]),
@@ -452,7 +488,10 @@ void build_graph(rhp_ctx& c) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
-  launch_iteration(c, 0, cap);
+  // the body runs kGraphUnroll iterations: one conditional evaluation (a
+  // device-side relaunch of the body) per kGraphUnroll K1/K2 pairs; copies
+  // after the first skip themselves once a K1 has stopped the block
+  for (int j = 0; j < kGraphUnroll; ++j) launch_iteration(c, j, cap, j > 0);
   cudaGraph_t g2;
   CK(cudaStreamEndCapture(cap, &g2));
   CK(cudaGraphInstantiate(&c.gexec, c.graph, 0));
@@ -578,7 +617,7 @@ int rhp_nccl_unique_id(void* out128) {
   return guarded([&] {
 #ifdef RHP_WITH_NCCL
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) throw CudaError("ncclGetUniqueId failed");
+    if (nccl().GetUniqueId(&id) != ncclSuccess) throw CudaError("ncclGetUniqueId failed");
     std::memcpy(out128, &id, sizeof(id));
 #else
     (void)out128;
@@ -709,7 +748,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
 #ifdef RHP_WITH_NCCL
       ncclUniqueId id;
       std::memcpy(&id, opt.nccl_id, sizeof(id));
-      if (ncclCommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess)
+      if (nccl().CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess)
         throw CudaError("ncclCommInitRank failed");
 #else
       throw CudaError("built without NCCL");
@@ -740,7 +779,7 @@ int rhp_destroy(rhp_ctx* c) {
   if (c->res_a_split) cudaFree(c->res_a_split);
   if (c->res_at_split) cudaFree(c->res_at_split);
 #ifdef RHP_WITH_NCCL
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) nccl().CommDestroy(c->comm);
 #endif
   if (c->ctl) cudaFree(c->ctl);
   if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -1042,7 +1081,7 @@ void gather_rows(rhp_ctx& c, const double* dev_local, double* host_full) {
   const size_t ml = static_cast<size_t>(c.m), mx = static_cast<size_t>(c.max_local);
   CK(cudaMemsetAsync(c.ypad, 0, std::max<size_t>(mx, 1) * sizeof(double), s));
   if (ml) CK(cudaMemcpyAsync(c.ypad, dev_local, ml * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (ncclAllGather(c.ypad, c.ygather, mx, ncclDouble, c.comm, s) != ncclSuccess)
+  if (nccl().AllGather(c.ypad, c.ygather, mx, ncclDouble, c.comm, s) != ncclSuccess)
     throw CudaError("ncclAllGather failed");
   std::vector<double> all(mx * static_cast<size_t>(c.world));
   if (!all.empty())
@@ -1087,7 +1126,7 @@ int rhp_any(rhp_ctx* c, int flag, int* any) {
 #ifdef RHP_WITH_NCCL
     int64_t v = flag ? 1 : 0;
     CK(cudaMemcpyAsync(c->agree, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
-    if (ncclAllReduce(c->agree, c->agree, 1, ncclInt64, ncclMax, c->comm, c->stream) != ncclSuccess)
+    if (nccl().AllReduce(c->agree, c->agree, 1, ncclInt64, ncclMax, c->comm, c->stream) != ncclSuccess)
       throw CudaError("ncclAllReduce(agree) failed");
     CK(cudaMemcpyAsync(&v, c->agree, sizeof v, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

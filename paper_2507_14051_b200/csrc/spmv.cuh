@@ -47,6 +47,15 @@ __device__ __forceinline__ int sv(int64_t e) {
   return static_cast<int>((u % kPer) * 32u + u / kPer);
 }
 
+// Position type of the warp walk (RHP_IDX32: 32-bit, see warp_range).
+#if RHP_IDX32
+using ix = int32_t;
+constexpr ix kIxMax = INT32_MAX;
+#else
+using ix = int64_t;
+constexpr ix kIxMax = INT64_MAX;
+#endif
+
 struct WarpSmem {
   double val[kWin];          // products, then segmented-scan values
   unsigned char flag[kWin];  // 1 where a row starts
@@ -114,29 +123,32 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
                                            const double* __restrict__ xg, const Sched& s,
                                            Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
   const int lane = threadIdx.x & 31;
-  const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  const int w = static_cast<int>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   if (w >= s.n_warps) return;
+  // row and nonzero positions fit 32 bits (ingest.cu caps an operator at
+  // 2^31 - 2^16 nonzeros): 32-bit locals halve their registers and shuffles
   const int64_t* rp = s.rp;
-  const int64_t row_head = s.warp_row[w], r_end = s.warp_row[w + 1];
-  const int64_t e0 = s.warp_nz[w], e_end = s.warp_nz[w + 1];
+  const ix row_head = static_cast<ix>(s.warp_row[w]), r_end = static_cast<ix>(s.warp_row[w + 1]);
+  const ix e0 = static_cast<ix>(s.warp_nz[w]), e_end = static_cast<ix>(s.warp_nz[w + 1]);
   const int hslot = s.head_slot[w];
-  const int64_t r_lim = r_end < s.rows ? r_end + 1 : s.rows;  // rows whose end may be read
-  int64_t r = row_head;
-  int64_t rstart = rp[r];  // start of row r (warp-uniform)
+  const ix rows = static_cast<ix>(s.rows);
+  const ix r_lim = r_end < rows ? r_end + 1 : rows;  // rows whose end may be read
+  ix r = row_head;
+  ix rstart = static_cast<ix>(rp[r]);  // start of row r (warp-uniform)
   double carry = 0.0;
   // windows are aligned to 4 nonzeros (16-B vector loads); elements outside
   // [e0, e_end) are masked to zero
-  int64_t wb = e0 & ~int64_t(3);
+  ix wb = e0 & ~ix(3);
   int cn[kPer];  // column indices of this lane's elements of the current window
   if constexpr (!WALK) {
     if (wb + kPer * lane < e_end) ld_idx(ci, wb + kPer * lane, cn);
   }
   for (;; wb += kWin) {
-    const int64_t we = wb + kWin < e_end ? wb + kWin : e_end;  // valid end of the window
+    const ix we = wb + kWin < e_end ? wb + kWin : e_end;  // valid end of the window
     // ends of the next 32 rows: group 0 of the flags and of the completion pass
-    int64_t re0 = r + lane < r_lim ? rp[r + lane + 1] : INT64_MAX;
+    ix re0 = r + lane < r_lim ? static_cast<ix>(rp[r + lane + 1]) : kIxMax;
     if constexpr (!WALK) {
-      const int64_t mine = wb + kPer * lane;  // first element of this lane
+      const ix mine = wb + kPer * lane;  // first element of this lane
       // (1) values and gathers of this window, then the next window's indices
       double p[kPer], vc[kPer];
       if (mine < we) ld_vals(vals, mine, vc);
@@ -156,11 +168,11 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
       for (int h = 0; h < kPer / 4; ++h) reinterpret_cast<uint32_t*>(sm.flag)[lane * (kPer / 4) + h] = 0u;
       __syncwarp();
       if (lane == 0 && rstart >= wb && rstart < we) sm.flag[rstart - wb] = 1;
-      for (int64_t g = r, re = re0;;) {
+      for (ix g = r, re = re0;;) {
         if (re >= wb && re < we) sm.flag[re - wb] = 1;
         if (__shfl_sync(0xffffffffu, re, 31) >= we) break;
         g += 32;
-        re = g + lane < r_lim ? rp[g + lane + 1] : INT64_MAX;
+        re = g + lane < r_lim ? static_cast<ix>(rp[g + lane + 1]) : kIxMax;
       }
 #pragma unroll
       for (int t = 0; t < kPer; ++t) p[t] = mul(vc[t], p[t]);
@@ -201,11 +213,11 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
       __syncwarp();
     }
     // (4) rows ending in this window
-    for (int64_t re = re0;;) {
-      const int64_t row = r + lane;
+    for (ix re = re0;;) {
+      const ix row = r + lane;
       const bool inr = row < r_end;
-      if (!inr) re = INT64_MAX;
-      int64_t rs = __shfl_up_sync(0xffffffffu, re, 1);
+      if (!inr) re = kIxMax;
+      ix rs = __shfl_up_sync(0xffffffffu, re, 1);
       if (lane == 0) rs = rstart;
       const bool done = inr && re <= we;
       if (done) {
@@ -222,7 +234,7 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
 #pragma unroll
             for (int q = 0; q < Epi::NRED; ++q) s.long_red[(size_t)hslot * 16 + q] = la[q];
           } else {
-            contribute(s, epi, hslot, 2 * w, sum);
+            contribute(s, epi, hslot, 2 * static_cast<int64_t>(w), sum);
           }
         } else {
           load_inputs(epi, row, ein);
@@ -233,7 +245,7 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
       if (nc > 0) rstart = __shfl_sync(0xffffffffu, re, nc - 1);  // end of the last finished row
       r += nc;
       if (nc < 32) break;
-      re = r + lane < r_end ? rp[r + lane + 1] : INT64_MAX;
+      re = r + lane < r_end ? static_cast<ix>(rp[r + lane + 1]) : kIxMax;
     }
     if constexpr (!WALK) {
       // partial sum of the row left open at the window's end
@@ -245,8 +257,8 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
   if constexpr (!WALK) {
     // the range ends inside row r_end: contribute its partial
     if (lane == 0 && r_end < s.rows && e_end > rstart) {
-      if (r_end == row_head && hslot >= 0) contribute(s, epi, hslot, 2 * w, carry);
-      else contribute(s, epi, s.tail_slot[w], 2 * w + 1, carry);
+      if (r_end == row_head && hslot >= 0) contribute(s, epi, hslot, 2 * static_cast<int64_t>(w), carry);
+      else contribute(s, epi, s.tail_slot[w], 2 * static_cast<int64_t>(w) + 1, carry);
     }
   }
 }

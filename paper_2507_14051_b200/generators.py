@@ -12,6 +12,7 @@ to the variable type so the LP is dual feasible (bounded).
     c3_transport(seed, S, T)  S supplies x T demands, n=S*T, nnz=2n (rows of length T and S)
     c4_multicommodity(...)    K commodities on a random graph, conservation
                               equalities + [0, cap] capacity rows
+    c5_rowpart(...)           m=50M, n=20M, ~1B nnz (GPU-generated, gen_device.py)
 Generation is vectorised numpy with numpy.random.Generator(PCG64(seed)).
 """
 from __future__ import annotations
@@ -161,9 +162,18 @@ def c4_multicommodity(seed: int = 20240821, V: int = 200_000, E: int = 1_000_000
                      name="c4_multicommodity")
 
 
+def c5_rowpart(**kw) -> LpProblem:
+    """C5: ~1B-nonzero C2-like LP (m=50M, n=20M), generated on the GPU
+    (gen_device.py: a host numpy build of 1B nonzeros is impractical)."""
+    from .gen_device import c5_rowpart as gen
+
+    return gen(**kw)
+
+
 CONFIGS = {
     "c1": c1_small,
     "c2": c2_powerlaw,
     "c3": c3_transport,
     "c4": c4_multicommodity,
+    "c5": c5_rowpart,
 }

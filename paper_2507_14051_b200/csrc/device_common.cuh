@@ -33,7 +33,7 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kMinBlocks = RHP_MIN_BLOCKS;  // resident CTAs per SM the SpMV is built for
 constexpr int kPer = RHP_WIN_PER;           // nonzeros per lane per window
 constexpr int kWin = 32 * kPer;             // nonzeros per warp window
-static_assert(kPer == 4 || kPer == 8, "window of 4 or 8 nonzeros per lane");
+static_assert(kPer == 4 || kPer == 8 || kPer == 16, "window of 4, 8 or 16 nonzeros per lane");
 // Cost of a row in nonzeros when balancing warp ranges (row pointer, flags,
 // epilogue inputs and outputs vs index, value and gather per nonzero).
 #ifndef RHP_ROW_WEIGHT

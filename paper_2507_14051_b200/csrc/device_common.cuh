@@ -88,6 +88,13 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 #define RHP_IDX32 1
 #endif
 
+// Target cost (nonzeros + 3 rows) of one merge-path chunk: an operator gets
+// max(1, cost / (warps * kChunkCost)) chunks per warp.
+#ifndef RHP_CHUNK_COST
+#define RHP_CHUNK_COST 4096
+#endif
+constexpr int kChunkCost = RHP_CHUNK_COST;
+
 // K1/K2 pairs per body of the block graph's WHILE node.
 #ifndef RHP_GRAPH_UNROLL
 #define RHP_GRAPH_UNROLL 2
@@ -122,26 +129,28 @@ struct Ctl {
   double* hist;                    // [block_limit] residual history of the current block
 };
 
-// Operator schedule (built by layout.cu for a given warp count): warp w owns
-// the merge-path range that starts at row warp_row[w], nonzero warp_nz[w]
-// and ends where warp w+1 starts (rows + nonzeros balanced, boundaries snapped
-// to row starts except inside long rows). A row cut by one or more range
-// boundaries is a "split row" with a slot: every warp that touches it stores
-// its partial sum, and the last one to arrive adds them in warp order and runs
-// the row's epilogue (reductions into long_red[slot]).
+// Operator schedule (built by layout.cu for a given warp count): chunk c is
+// the merge-path range that starts at row warp_row[c], nonzero warp_nz[c]
+// and ends where chunk c+1 starts (rows + nonzeros balanced, boundaries
+// snapped to row starts except inside long rows); warp w walks chunks w,
+// w + n_warps, ... A row cut by one or more chunk boundaries is a "split row"
+// with a slot: every chunk that touches it stores its partial sum, and the
+// last one to arrive adds them in chunk order and runs the row's epilogue
+// (reductions into long_red[slot]).
 struct Sched {
   int32_t n_multi;            // split rows (slots)
-  int32_t n_warps;            // warps the ranges were built for (grid * kWarps)
+  int32_t n_warps;            // warps of the grid the schedule was built for (grid * kWarps)
+  int32_t n_chunks;           // merge-path chunks (a multiple of n_warps); warp w walks w, w+W, ...
   int64_t rows;
   const int64_t* rp;          // the operator's row pointers
-  const int64_t* warp_row;    // [n_warps + 1]
-  const int64_t* warp_nz;     // [n_warps + 1]
-  const int32_t* head_slot;   // [n_warps] slot of warp_row[w] when the range starts inside it, else -1
-  const int32_t* tail_slot;   // [n_warps] slot of the row the range ends inside, else -1
+  const int64_t* warp_row;    // [n_chunks + 1] first row of chunk c
+  const int64_t* warp_nz;     // [n_chunks + 1] first nonzero of chunk c
+  const int32_t* head_slot;   // [n_chunks] slot of warp_row[c] when the chunk starts inside it, else -1
+  const int32_t* tail_slot;   // [n_chunks] slot of the row the chunk ends inside, else -1
   const int64_t* slot_row;    // [n_multi]
-  const int32_t* slot_first;  // [n_multi] first contributing warp (it holds the row's start)
+  const int32_t* slot_first;  // [n_multi] first contributing chunk (it holds the row's start)
   const int32_t* slot_count;  // [n_multi] contributing warps (consecutive)
-  double* slot_part;          // [2 * n_warps] per warp: head partial, tail partial
+  double* slot_part;          // [2 * n_chunks] per chunk: head partial, tail partial
   unsigned int* slot_ticket;  // [n_multi]
   double* long_red;           // [n_multi * 16] epilogue reductions of split rows
 };

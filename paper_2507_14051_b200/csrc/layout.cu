@@ -24,8 +24,14 @@ namespace rhp {
 // 1000-nonzero rows: K1 33 -> 23 us), in which case the row is split there.
 // Consecutive boundaries inside one row share its slot.
 void build_schedule(HostOperator& op, int64_t n_warps, double row_weight) {
-  const int64_t W = std::max<int64_t>(1, n_warps);
+  const int64_t NW = std::max<int64_t>(1, n_warps);
   const int64_t R = op.rows, Z = op.nnz;
+  // chunks per warp: ~kChunkCost of work each (warp w walks chunks w, w+NW, ...)
+  const double work = static_cast<double>(Z) + row_weight * static_cast<double>(R);
+  const int64_t cpw = std::max<int64_t>(
+      1, std::min<int64_t>(static_cast<int64_t>(work / (static_cast<double>(NW) * kChunkCost)),
+                           (INT32_MAX / 2) / NW));
+  const int64_t W = NW * cpw;  // chunks
   const std::vector<int64_t>& rp = op.rp;
   for (int k = 0; k < 8; ++k) op.bin_rows[k] = 0;
   for (int64_t r = 0; r < R; ++r) op.bin_rows[row_kind(rp[r + 1] - rp[r])]++;
@@ -94,7 +100,8 @@ void build_schedule(HostOperator& op, int64_t n_warps, double row_weight) {
   Sched& s = op.sched;
   s = Sched{};
   s.n_multi = static_cast<int32_t>(op.slot_row.size());
-  s.n_warps = static_cast<int32_t>(W);
+  s.n_warps = static_cast<int32_t>(NW);
+  s.n_chunks = static_cast<int32_t>(W);
   s.rows = R;
 }
 

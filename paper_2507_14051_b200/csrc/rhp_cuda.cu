@@ -177,7 +177,7 @@ int occupancy_blocks(const void* fn) {
 
 // Uploads the warp schedule of an operator (built for the operator's grid).
 void upload_sched(DevOp& d, const HostOperator& h, cudaStream_t s) {
-  const size_t W = static_cast<size_t>(h.sched.n_warps), ns = h.slot_row.size();
+  const size_t W = static_cast<size_t>(h.sched.n_chunks), ns = h.slot_row.size();
   d.warp_row = dev_alloc<int64_t>(W + 1);
   d.warp_nz = dev_alloc<int64_t>(W + 1);
   d.head_slot = dev_alloc<int32_t>(W);

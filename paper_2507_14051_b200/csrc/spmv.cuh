@@ -117,14 +117,13 @@ __device__ __forceinline__ void contribute(const Sched& s, Epi& epi, int slot, i
   s.slot_ticket[slot] = 0u;
 }
 
-// One warp's range. WALK: epilogue only (row sums 0), same row -> lane map.
+// One merge-path chunk w, walked by one warp. WALK: epilogue only (row sums
+// 0), same row -> lane map.
 template <class Epi, bool WALK>
-__device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals,
-                                           const double* __restrict__ xg, const Sched& s,
-                                           Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
+__device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, const double* vals,
+                                            const double* __restrict__ xg, const Sched& s,
+                                            Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
   const int lane = threadIdx.x & 31;
-  const int w = static_cast<int>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
-  if (w >= s.n_warps) return;
   // row and nonzero positions fit 32 bits (ingest.cu caps an operator at
   // 2^31 - 2^16 nonzeros): 32-bit locals halve their registers and shuffles
   const int64_t* rp = s.rp;
@@ -261,6 +260,20 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
       else contribute(s, epi, s.tail_slot[w], 2 * static_cast<int64_t>(w) + 1, carry);
     }
   }
+}
+
+// A warp walks the chunks w, w + W, w + 2W, ... (W = warps of the grid): at
+// any moment the whole grid works on one band of consecutive chunks, so the
+// columns those rows gather from form a narrow working set in L2 whenever
+// the matrix has row locality (C4: one commodity's 8 MB slice of x instead of
+// all 160 MB). The epilogue reductions accumulate over the warp's chunks.
+template <class Epi, bool WALK>
+__device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals,
+                                           const double* __restrict__ xg, const Sched& s,
+                                           Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
+  const int w = static_cast<int>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  for (int c = w; c < s.n_chunks; c += s.n_warps)
+    chunk_range<Epi, WALK>(c, ci, vals, xg, s, epi, acc, sm);
 }
 
 // Epi provides: NRED (>= 1) reductions, NIN per-row input vectors `in[NIN]`,

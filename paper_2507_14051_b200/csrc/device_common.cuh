@@ -88,12 +88,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 #define RHP_IDX32 1
 #endif
 
-// Target cost (nonzeros + 3 rows) of one merge-path chunk: an operator gets
-// max(1, cost / (warps * kChunkCost)) chunks per warp.
+// Target cost (nonzeros + 3 rows) of one merge-path chunk when the gathered
+// vector exceeds kGatherL2Bytes: max(1, cost / (warps * kChunkCost)) chunks
+// per warp (layout.cu build_schedule).
 #ifndef RHP_CHUNK_COST
-#define RHP_CHUNK_COST 4096
+#define RHP_CHUNK_COST 2048
 #endif
 constexpr int kChunkCost = RHP_CHUNK_COST;
+constexpr double kGatherL2Bytes = 32.0 * 1024 * 1024;
 
 // K1/K2 pairs per body of the block graph's WHILE node.
 #ifndef RHP_GRAPH_UNROLL

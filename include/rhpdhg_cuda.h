@@ -131,6 +131,8 @@ typedef struct rhp_layout_info {
   int64_t col_bins[8];  /* rows of A^T per bin */
   int32_t grid_a, grid_at, grid_vec;
   int32_t sm_count;
+  int32_t gather_l1;    /* bit 0: A's SpMV gathers through L1, bit 1: A^T's (tuned at create) */
+  int32_t pdl;          /* SpMVs use programmatic dependent launch */
 } rhp_layout_info;
 
 const char* rhp_last_error(void);

@@ -62,11 +62,17 @@ __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p);
 __device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
 __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((const long long*)p); }
 
-// Random gather of the SpMV input vector (L2 resident, almost never an L1 hit).
+// Gather of the SpMV input vector. Default: L1::no_allocate — a random
+// gather over a vector much larger than L1 almost never hits, and allocating
+// evicts useful lines. L1G (chosen per operator by timing both at setup,
+// rhp_cuda.cu tune_gathers): the read-only L1-allocating path, for vectors
+// that fit L1 (C3's A^T gathers a 16 KB y) or columns clustered within rows.
 #ifndef RHP_GATHER_MODE
 #define RHP_GATHER_MODE 2
 #endif
+template <bool L1G = false>
 __device__ __forceinline__ double ld_gather(const double* p) {
+  if constexpr (L1G) return __ldg(p);  // L1-allocating: small or clustered vectors
 #if RHP_GATHER_MODE == 1
   return __ldcg(p);  // L2 only
 #elif RHP_GATHER_MODE == 2
@@ -76,6 +82,16 @@ __device__ __forceinline__ double ld_gather(const double* p) {
 #else
   return __ldg(p);  // read-only path
 #endif
+}
+
+// Programmatic dependent launch (launch_spmv sets the attribute): wait until
+// the preceding kernel has completed and its writes are visible (a no-op when
+// launched without the attribute), then let the next kernel's CTAs be
+// scheduled as this grid's CTAs retire, so its launch latency overlaps this
+// kernel's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Bulk L2 prefetch (address and size multiples of 16 B; no completion).

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -113,6 +114,7 @@ struct DevOp : DeviceCsr {
   int32_t *head_slot = nullptr, *tail_slot = nullptr, *slot_first = nullptr, *slot_count = nullptr;
   double *slot_part = nullptr, *long_red = nullptr;
   unsigned int* slot_ticket = nullptr;
+  bool l1g = false;  // L1-allocating gathers (tune_gathers)
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
 
@@ -162,6 +164,7 @@ struct rhp_ctx {
   int res_ctas = 1, res_wa = 1, res_wat = 1;
   size_t res_smem = 0;
   int32_t *res_a_split = nullptr, *res_at_split = nullptr;
+  bool pdl = false;  // programmatic dependent launch of the SpMVs (launch_spmv, RHP_PDL=1)
 #ifdef RHP_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -250,20 +253,37 @@ int vec_grid(const rhp_ctx& c, int64_t len) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)c.sm_count * 8)));
 }
 
+// With RHP_PDL=1 every SpMV is launched with programmatic stream
+// serialization: spmv_fused waits for its predecessor with
+// griddepcontrol.wait, so its launch and CTA rasterisation overlap the
+// predecessor's tail. Off by default: measured inside the block graph it
+// gains nothing on C2 (6904 vs 6895 iter/s) and loses 6% on C3 (20.1k vs
+// 18.9k) — the graph already launches the next kernel back to back.
 template <class Epi>
 void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
                  double* part, unsigned int* ticket, cudaStream_t s) {
-  (void)c;
-  spmv_fused<Epi><<<grid, kBlock, 0, s>>>(op.csr(), xg, op.sched, epi, part, ticket);
-  CK(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = c.pdl ? 1 : 0;
+  if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
+  else CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
 }
 
 // Resident CTAs per SM of an SpMV instantiation.
 template <class Epi>
 int prepare_spmv() {
-  const void* fn = reinterpret_cast<const void*>(spmv_fused<Epi>);
-  int b = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
+  int b = 0, b1 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b, reinterpret_cast<const void*>(spmv_fused<Epi, false>), kBlock, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b1, reinterpret_cast<const void*>(spmv_fused<Epi, true>), kBlock, 0));
+  b = std::min(b, b1);
   if (b < 1) throw CudaError("spmv kernel does not fit on an SM");
   return b;
 }
@@ -274,6 +294,42 @@ EpiStore store_into(double* out) {
   EpiStore e{};
   e.out = out;
   return e;
+}
+
+// Gather cache policy per operator (ld_gather): RHP_L1_GATHER=0/1 forces it;
+// otherwise both variants of the plain SpMV are timed once at setup (one
+// warm-up, then the best of `reps`) and the faster is kept. The policy only
+// changes which cache the gathered values pass through, never a result.
+// Measured: C2 keeps no_allocate on both operators (random columns over an
+// 8 MB / 4 MB vector); C3's A^T (16 KB y) and both C4 operators (columns
+// clustered per commodity / edge) take L1: C4 718 -> 844 iter/s.
+void tune_gathers(rhp_ctx& c) {
+  const char* env = std::getenv("RHP_L1_GATHER");
+  if (env && (env[0] == '0' || env[0] == '1')) {
+    c.A.l1g = c.At.l1g = env[0] == '1';
+    return;
+  }
+  struct Case { DevOp* op; int grid; const double* in; double* out; };
+  const Case cases[2] = {{&c.A, c.grid_a, c.pv, c.pav}, {&c.At, c.grid_at, c.pav, c.pw}};
+  for (const Case& k : cases) {
+    if (k.op->nnz == 0) continue;
+    const int reps = k.op->nnz > (int64_t)100000000 ? 3 : 6;
+    float best[2] = {1e30f, 1e30f};
+    for (int variant = 0; variant < 2; ++variant) {
+      k.op->l1g = variant == 1;
+      launch_spmv(c, *k.op, k.grid, k.in, store_into(k.out), nullptr, nullptr, c.stream);
+      for (int r = 0; r < reps; ++r) {
+        CK(cudaEventRecord(c.tev0, c.stream));
+        launch_spmv(c, *k.op, k.grid, k.in, store_into(k.out), nullptr, nullptr, c.stream);
+        CK(cudaEventRecord(c.tev1, c.stream));
+        CK(cudaEventSynchronize(c.tev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c.tev0, c.tev1));
+        best[variant] = std::min(best[variant], ms);
+      }
+    }
+    k.op->l1g = best[1] < 0.99f * best[0];  // ties keep no_allocate
+  }
 }
 
 EpiDual epi_dual(rhp_ctx& c, int token) {
@@ -720,6 +776,8 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     for (double** p2 : {&c->part1, &c->part3, &c->partA, &c->partAt})
       *p2 = dev_alloc<double>(static_cast<size_t>(c->grid_max) * 16);
     c->hist = dev_alloc<double>(static_cast<size_t>(opt.block_limit));
+    if (const char* e = std::getenv("RHP_PDL")) c->pdl = e[0] == '1';
+    tune_gathers(*c);
     CK(cudaMalloc(&c->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));
     std::memset(c->ctl_host, 0, sizeof(Ctl));
@@ -806,6 +864,8 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->grid_at = c->grid_at;
     info->grid_vec = c->grid_vec;
     info->sm_count = c->sm_count;
+    info->gather_l1 = (c->A.l1g ? 1 : 0) | (c->At.l1g ? 2 : 0);
+    info->pdl = c->pdl ? 1 : 0;
   });
 }
 

@@ -119,7 +119,7 @@ __device__ __forceinline__ void contribute(const Sched& s, Epi& epi, int slot, i
 
 // One merge-path chunk w, walked by one warp. WALK: epilogue only (row sums
 // 0), same row -> lane map.
-template <class Epi, bool WALK>
+template <class Epi, bool WALK, bool L1G = false>
 __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, const double* vals,
                                             const double* __restrict__ xg, const Sched& s,
                                             Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
@@ -155,9 +155,9 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
       for (int t = 0; t < kPer; ++t) {
         const bool ok = mine + t >= e0 && mine + t < we;
 #ifdef RHP_FAKE_GATHER  // timing experiment only: gathers confined to 32 KB of x (L1 hits)
-        p[t] = ok ? ld_gather(xg + (cn[t] & 0xfff)) : 0.0;
+        p[t] = ok ? ld_gather<L1G>(xg + (cn[t] & 0xfff)) : 0.0;
 #else
-        p[t] = ok ? ld_gather(xg + cn[t]) : 0.0;
+        p[t] = ok ? ld_gather<L1G>(xg + cn[t]) : 0.0;
 #endif
         if (!ok) vc[t] = 0.0;
       }
@@ -267,30 +267,33 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
 // columns those rows gather from form a narrow working set in L2 whenever
 // the matrix has row locality (C4: one commodity's 8 MB slice of x instead of
 // all 160 MB). The epilogue reductions accumulate over the warp's chunks.
-template <class Epi, bool WALK>
+template <class Epi, bool WALK, bool L1G = false>
 __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals,
                                            const double* __restrict__ xg, const Sched& s,
                                            Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
   const int w = static_cast<int>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   for (int c = w; c < s.n_chunks; c += s.n_warps)
-    chunk_range<Epi, WALK>(c, ci, vals, xg, s, epi, acc, sm);
+    chunk_range<Epi, WALK, L1G>(c, ci, vals, xg, s, epi, acc, sm);
 }
 
+// L1G: L1-allocating gathers (ld_gather).
 // Epi provides: NRED (>= 1) reductions, NIN per-row input vectors `in[NIN]`,
 // REDUCE, FINAL; bool enter() (block-uniform early exit); void row(int64_t
 // i, double rowsum, const double* e, int stride, double(&acc)[NRED]) with
 // input k of row i at e[k*stride]; and, when FINAL, void finalize(const
 // Sched&, const double* part, int grid) (last block).
-template <class Epi>
+template <class Epi, bool L1G = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const double* __restrict__ xg,
                                                                  Sched s, Epi epi, double* part,
                                                                  unsigned int* ticket) {
+  pdl_wait();
+  pdl_trigger();
   if (!epi.enter()) return;
   __shared__ __align__(16) WarpSmem wsm[kWarps];
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  warp_range<Epi, false>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
+  warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
   if constexpr (Epi::REDUCE) {
     block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
     if constexpr (Epi::FINAL) {
@@ -306,6 +309,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
 // assignment (row sum argument 0, inputs read from global memory).
 template <class Epi>
 __global__ void __launch_bounds__(kBlock) epilogue_walk(Sched s, Epi epi, double* part) {
+  pdl_wait();
+  pdl_trigger();
   if (!epi.enter()) return;
   __shared__ __align__(16) WarpSmem wsm[kWarps];
   double acc[Epi::NRED];

@@ -264,7 +264,9 @@ int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
     o[20] = li.grid_at;
     o[21] = li.grid_vec;
     o[22] = li.sm_count;
-    o[23] = o[24] = o[25] = o[26] = 0;
+    o[23] = li.gather_l1;
+    o[24] = li.pdl;
+    o[25] = o[26] = 0;
   });
 }
 

@@ -194,7 +194,8 @@ int rhpdhg_session_time_kernels(rhpdhg_session* s, int reps, double* ms3);
 /* Device layout summary: m, n, nnz, then rows of A and of A^T per schedule
  * bin (8 each), the grids of the A, A^T and vector kernels, the SM count,
  * the gather cache policy (bit 0: A through L1, bit 1: A^T) and whether the
- * SpMVs use programmatic dependent launch. */
+ * SpMVs use programmatic dependent launch, then the engine bits (bit 0: A
+ * uses the thread-per-row engine, bit 1: A^T). */
 int rhpdhg_session_layout(rhpdhg_session* s, int64_t* out27);
 int rhpdhg_session_finish(rhpdhg_session* s, rhpdhg_report_c* report, double* x, double* y,
                           double* reduced_costs, double* history, int64_t history_cap);

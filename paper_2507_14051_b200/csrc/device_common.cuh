@@ -113,6 +113,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 constexpr int kChunkCost = RHP_CHUNK_COST;
 constexpr double kGatherL2Bytes = 32.0 * 1024 * 1024;
 
+// Operators whose longest row has at most kThreadRowMax nonzeros use the
+// thread-per-row engine (spmv.cuh thread_rows; rhp_cuda.cu choose_engines).
+constexpr int64_t kThreadRowMax = 8;
+
 // K1/K2 pairs per body of the block graph's WHILE node.
 #ifndef RHP_GRAPH_UNROLL
 #define RHP_GRAPH_UNROLL 2
@@ -156,6 +160,7 @@ struct Ctl {
 // last one to arrive adds them in chunk order and runs the row's epilogue
 // (reductions into long_red[slot]).
 struct Sched {
+  int32_t thread_rows;        // 1: thread-per-row engine (spmv.cuh thread_rows), no chunks or slots
   int32_t n_multi;            // split rows (slots)
   int32_t n_warps;            // warps of the grid the schedule was built for (grid * kWarps)
   int32_t n_chunks;           // merge-path chunks (a multiple of n_warps); warp w walks w, w+W, ...

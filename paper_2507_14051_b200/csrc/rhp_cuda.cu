@@ -296,6 +296,23 @@ EpiStore store_into(double* out) {
   return e;
 }
 
+// SpMV engine per operator (deterministic, from the row lengths only, so two
+// contexts on one LP always agree bit for bit): thread-per-row when the
+// longest row has <= kThreadRowMax nonzeros, else the merge-path warp engine.
+// RHP_THREAD_ROWS=0 forces merge path; =1 allows rows up to 64 nonzeros.
+void choose_engines(rhp_ctx& c) {
+  const char* env = std::getenv("RHP_THREAD_ROWS");
+  const int64_t cap = env && env[0] == '0' ? -1 : env && env[0] == '1' ? 64 : kThreadRowMax;
+  for (auto [d, h] : {std::pair<DevOp*, const HostOperator*>{&c.A, &c.L.A}, {&c.At, &c.L.At}}) {
+    int64_t longest = 0;
+    for (int64_t r = 0; r < h->rows; ++r) longest = std::max(longest, h->rp[r + 1] - h->rp[r]);
+    if (h->rows > 0 && longest <= cap) {
+      d->sched.thread_rows = 1;
+      d->sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
+    }
+  }
+}
+
 // Gather cache policy per operator (ld_gather): RHP_L1_GATHER=0/1 forces it;
 // otherwise both variants of the plain SpMV are timed once at setup (one
 // warm-up, then the best of `reps`) and the faster is kept. The policy only
@@ -313,22 +330,20 @@ void tune_gathers(rhp_ctx& c) {
   const Case cases[2] = {{&c.A, c.grid_a, c.pv, c.pav}, {&c.At, c.grid_at, c.pav, c.pw}};
   for (const Case& k : cases) {
     if (k.op->nnz == 0) continue;
-    const int reps = k.op->nnz > (int64_t)100000000 ? 3 : 6;
+    const int reps = k.op->nnz > (int64_t)100000000 ? 3 : 8;
     float best[2] = {1e30f, 1e30f};
-    for (int variant = 0; variant < 2; ++variant) {
-      k.op->l1g = variant == 1;
-      launch_spmv(c, *k.op, k.grid, k.in, store_into(k.out), nullptr, nullptr, c.stream);
-      for (int r = 0; r < reps; ++r) {
+    for (int r = -1; r < reps; ++r)  // variants alternate, so drift hits both; r = -1 warms up
+      for (int variant = 0; variant < 2; ++variant) {
+        k.op->l1g = variant == 1;
         CK(cudaEventRecord(c.tev0, c.stream));
         launch_spmv(c, *k.op, k.grid, k.in, store_into(k.out), nullptr, nullptr, c.stream);
         CK(cudaEventRecord(c.tev1, c.stream));
         CK(cudaEventSynchronize(c.tev1));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, c.tev0, c.tev1));
-        best[variant] = std::min(best[variant], ms);
+        if (r >= 0) best[variant] = std::min(best[variant], ms);
       }
-    }
-    k.op->l1g = best[1] < 0.99f * best[0];  // ties keep no_allocate
+    k.op->l1g = best[1] < 0.97f * best[0];  // L1 only on a clear win
   }
 }
 
@@ -777,6 +792,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       *p2 = dev_alloc<double>(static_cast<size_t>(c->grid_max) * 16);
     c->hist = dev_alloc<double>(static_cast<size_t>(opt.block_limit));
     if (const char* e = std::getenv("RHP_PDL")) c->pdl = e[0] == '1';
+    choose_engines(*c);
     tune_gathers(*c);
     CK(cudaMalloc(&c->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));
@@ -866,6 +882,7 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->sm_count = c->sm_count;
     info->gather_l1 = (c->A.l1g ? 1 : 0) | (c->At.l1g ? 2 : 0);
     info->pdl = c->pdl ? 1 : 0;
+    info->thread_rows = (c->A.sched.thread_rows ? 1 : 0) | (c->At.sched.thread_rows ? 2 : 0);
   });
 }
 

@@ -276,6 +276,62 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
     chunk_range<Epi, WALK, L1G>(c, ci, vals, xg, s, epi, acc, sm);
 }
 
+// Thread-per-row engine, for operators whose rows are all short
+// (Sched::thread_rows: max row length <= kThreadRowMax, chosen at setup —
+// C3's A^T rows have 2 nonzeros, C4's 3). Thread g of the grid owns rows g,
+// g + G, g + 2G, ... (G = threads of the grid), two rows in flight per
+// thread. No scan, no shared memory and no split rows: a row's products are
+// summed sequentially in element order — the reference's own order
+// (sparse_matrix.cpp:67-87), so these row sums are bit-identical to its — and
+// the epilogue inputs, independent of the sum, are loaded first, so a row
+// costs one dependent chain (row pointers -> indices -> gathers) with its
+// epilogue loads in its shadow. WALK: epilogue only, same row -> thread map.
+template <class Epi, bool WALK, bool L1G = false>
+__device__ __forceinline__ void thread_rows(const int32_t* ci, const double* vals,
+                                            const double* __restrict__ xg, const Sched& s,
+                                            Epi& epi, double (&acc)[Epi::NRED]) {
+  constexpr int NI = Epi::NIN > 0 ? Epi::NIN : 1;
+  const int64_t G = static_cast<int64_t>(gridDim.x) * kBlock;
+  const int64_t R = s.rows;
+  for (int64_t i1 = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x; i1 < R; i1 += 2 * G) {
+    const int64_t i2 = i1 + G;
+    const bool two = i2 < R;
+    double e1[NI], e2[NI];
+    load_inputs(epi, i1, e1);
+    if (two) load_inputs(epi, i2, e2);
+    double s1 = 0.0, s2 = 0.0;
+    if constexpr (!WALK) {
+      const int64_t lo1 = s.rp[i1], hi1 = s.rp[i1 + 1];
+      const int64_t lo2 = two ? s.rp[i2] : 0, hi2 = two ? s.rp[i2 + 1] : 0;
+      const int64_t len = max(hi1 - lo1, hi2 - lo2);
+      for (int64_t t = 0; t < len; t += 4) {
+        int c1[4], c2[4];
+        double v1[4], v2[4], g1[4], g2[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok1 = lo1 + t + u < hi1, ok2 = lo2 + t + u < hi2;
+          c1[u] = ok1 ? __ldcs(ci + lo1 + t + u) : 0;
+          v1[u] = ok1 ? __ldcs(vals + lo1 + t + u) : 0.0;
+          c2[u] = ok2 ? __ldcs(ci + lo2 + t + u) : 0;
+          v2[u] = ok2 ? __ldcs(vals + lo2 + t + u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          g1[u] = lo1 + t + u < hi1 ? ld_gather<L1G>(xg + c1[u]) : 0.0;
+          g2[u] = lo2 + t + u < hi2 ? ld_gather<L1G>(xg + c2[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (lo1 + t + u < hi1) s1 = add(s1, mul(v1[u], g1[u]));
+          if (lo2 + t + u < hi2) s2 = add(s2, mul(v2[u], g2[u]));
+        }
+      }
+    }
+    epi.row(i1, s1, e1, 1, acc);
+    if (two) epi.row(i2, s2, e2, 1, acc);
+  }
+}
+
 // L1G: L1-allocating gathers (ld_gather).
 // Epi provides: NRED (>= 1) reductions, NIN per-row input vectors `in[NIN]`,
 // REDUCE, FINAL; bool enter() (block-uniform early exit); void row(int64_t
@@ -293,7 +349,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
+  if (s.thread_rows) thread_rows<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc);
+  else warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
   if constexpr (Epi::REDUCE) {
     block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
     if constexpr (Epi::FINAL) {
@@ -316,7 +373,8 @@ __global__ void __launch_bounds__(kBlock) epilogue_walk(Sched s, Epi epi, double
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  warp_range<Epi, true>(nullptr, nullptr, nullptr, s, epi, acc, wsm[threadIdx.x >> 5]);
+  if (s.thread_rows) thread_rows<Epi, true>(nullptr, nullptr, nullptr, s, epi, acc);
+  else warp_range<Epi, true>(nullptr, nullptr, nullptr, s, epi, acc, wsm[threadIdx.x >> 5]);
   block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
   epi.walk_done();
 }

@@ -459,7 +459,8 @@ class Session:
         return {"m": o[0], "n": o[1], "nnz": o[2], "row_bins": list(o[3:11]),
                 "col_bins": list(o[11:19]), "grid_a": o[19], "grid_at": o[20],
                 "grid_vec": o[21], "sm_count": o[22],
-                "gather_l1": {"A": bool(o[23] & 1), "At": bool(o[23] & 2)}, "pdl": bool(o[24])}
+                "gather_l1": {"A": bool(o[23] & 1), "At": bool(o[23] & 2)}, "pdl": bool(o[24]),
+                "thread_rows": {"A": bool(o[25] & 1), "At": bool(o[25] & 2)}}
 
     def finish(self) -> SolutionReport:
         def fn(view, cc, rep, x, y, rc_, hist, cap):

@@ -176,7 +176,10 @@ int rhpdhg_set_resident(int mode);
  * check; advance runs device blocks (with their KKT checks and restarts)
  * until at least `iterations` more PDHG iterations are done or the solve is
  * decided; finish completes the solve and fills the report like
- * rhpdhg_solve_csr. The session copies the LP. */
+ * rhpdhg_solve_csr. The session BORROWS the view's arrays (no host copy of
+ * the LP): they must stay valid and unchanged until rhpdhg_session_destroy.
+ * The matrix is validated by the device ingest with the same status codes
+ * and messages as rhpdhg_solve_csr. */
 typedef struct rhpdhg_session rhpdhg_session;
 int rhpdhg_session_create(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg,
                           rhpdhg_session** out);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -222,9 +223,23 @@ void free_op(DevOp& d) {
   d = DevOp{};
 }
 
+// First index of a contiguous ascending permutation (the layout keeps rows
+// and columns in their original order, so every map is one), else -1.
+int64_t contiguous_start(const std::vector<int32_t>& perm) {
+  for (size_t i = 1; i < perm.size(); ++i)
+    if (perm[i] != perm[i - 1] + 1) return -1;
+  return perm.empty() ? 0 : perm[0];
+}
+
 // gather a host vector in original order into device order
 void upload_perm(double* dst, const double* src, const std::vector<int32_t>& perm,
                  std::vector<double>& scratch, cudaStream_t s) {
+  const int64_t start = contiguous_start(perm);
+  if (start >= 0) {
+    upload(dst, src + start, perm.size(), s);
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
   scratch.resize(perm.size());
   for (size_t i = 0; i < perm.size(); ++i) scratch[i] = src[perm[i]];
   upload(dst, scratch.data(), scratch.size(), s);
@@ -233,6 +248,13 @@ void upload_perm(double* dst, const double* src, const std::vector<int32_t>& per
 
 void download_perm(double* dst, const double* src_dev, const std::vector<int32_t>& perm,
                    std::vector<double>& scratch, cudaStream_t s) {
+  const int64_t start = contiguous_start(perm);
+  if (start >= 0) {
+    if (!perm.empty())
+      CK(cudaMemcpyAsync(dst + start, src_dev, perm.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
   scratch.resize(perm.size());
   if (!perm.empty())
     CK(cudaMemcpyAsync(scratch.data(), src_dev, perm.size() * sizeof(double),
@@ -700,6 +722,16 @@ int rhp_nccl_unique_id(void* out128) {
 int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** out) {
   *out = nullptr;
   rhp_ctx* c = new rhp_ctx();
+  // RHPDHG_SETUP_TRACE=1: per-phase times of the context build on stderr
+  const bool trace = std::getenv("RHPDHG_SETUP_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  create %-22s %9.3f s\n", what, std::chrono::duration<double>(now - tp).count());
+    tp = now;
+  };
   const int rc = guarded([&] {
     rhp_options opt{};
     opt.device = 0;
@@ -740,8 +772,10 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
         c->max_local = std::max(c->max_local, c->offsets[r + 1] - c->offsets[r]);
       ingest_device(*lp, c->offsets[c->rank], c->offsets[c->rank + 1], c->L, c->A, c->At, c->stream);
     } else {
+      phase("device init");
       ingest_device(*lp, 0, lp->num_cons, c->L, c->A, c->At, c->stream);
     }
+    phase("ingest");
     const HostLayout& L = c->L;
     c->m = L.m;
     c->n = L.n;
@@ -784,8 +818,10 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     c->grid_at = clampg(c->L.At, (int64_t)c->sm_count * occ_at);
     build_schedule(c->L.A, (int64_t)c->grid_a * kWarps, kRowWeight);
     build_schedule(c->L.At, (int64_t)c->grid_at * kWarps, kRowWeight);
+    phase("vectors");
     upload_sched(c->A, c->L.A, s);
     upload_sched(c->At, c->L.At, s);
+    phase("schedules");
     c->grid_vec = vec_grid(*c, std::max<int64_t>(c->m, c->n));
     c->grid_max = std::max({c->grid_a, c->grid_at, c->grid_vec});
     for (double** p2 : {&c->part1, &c->part3, &c->partA, &c->partAt})
@@ -794,6 +830,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     if (const char* e = std::getenv("RHP_PDL")) c->pdl = e[0] == '1';
     choose_engines(*c);
     tune_gathers(*c);
+    phase("engines+gather tuning");
     CK(cudaMalloc(&c->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));
     std::memset(c->ctl_host, 0, sizeof(Ctl));
@@ -815,6 +852,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     // small LPs: one cluster runs whole blocks when its CSR slices fit in
     // shared memory (auto) or when forced
     c->resident = !c->dist && opt.resident != 0 && setup_resident(*c);
+    phase("resident check");
     if (c->dist) {
       c->ypad = dev_alloc<double>(static_cast<size_t>(c->max_local));
       c->ygather = dev_alloc<double>(static_cast<size_t>(c->max_local) * c->world);

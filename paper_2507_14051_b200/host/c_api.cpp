@@ -212,9 +212,18 @@ int rhpdhg_session_create(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg,
                           rhpdhg_session** out) {
   *out = nullptr;
   return guarded([&] {
+    if (!lp) throw UsageError("null LP view");
     auto h = std::make_unique<rhpdhg_session>();
-    h->problem = to_problem(lp);
-    h->session = std::make_unique<Session>(h->problem, to_config(cfg), default_device_options());
+    const bool complete = lp->num_cons >= 0 && lp->num_vars >= 0 &&
+                          (lp->num_cons == 0 || lp->row_ptr) &&
+                          (lp->num_cons == 0 || lp->row_ptr[lp->num_cons] == lp->row_ptr[0] ||
+                           (lp->col_index && lp->values));
+    if (complete) {  // zero-copy: the caller's arrays are borrowed until destroy
+      h->session = std::make_unique<Session>(*lp, to_config(cfg), default_device_options());
+    } else {
+      h->problem = to_problem(lp);
+      h->session = std::make_unique<Session>(h->problem, to_config(cfg), default_device_options());
+    }
     *out = h.release();
   });
 }

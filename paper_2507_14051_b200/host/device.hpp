@@ -26,6 +26,9 @@ inline void ok(int rc, const char* where) {
 }
 
 /// Borrowed C view of an LpProblem (CSR of its matrix).
+// LpProblem::validate's vector checks on a borrowed view (model.cpp).
+void validate_vectors(const rhpdhg_lp_view& v);
+
 inline rhpdhg_lp_view view_of(const LpProblem& p) {
   rhpdhg_lp_view v{};
   v.num_cons = p.num_cons();

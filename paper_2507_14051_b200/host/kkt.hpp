@@ -13,6 +13,7 @@ struct Denoms {
 };
 
 Denoms problem_denoms(const LpProblem& p);
+Denoms problem_denoms(const rhpdhg_lp_view& v);
 KktResiduals residuals_from_sums(const rhp_kkt_sums& s, const Denoms& d);
 
 }  // namespace rhpdhg::detail

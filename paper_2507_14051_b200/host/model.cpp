@@ -265,6 +265,16 @@ void LpProblem::validate() const {
   check_bounds(con_lb, con_ub, "constraint");
 }
 
+void detail::validate_vectors(const rhpdhg_lp_view& v) {
+  const size_t n = static_cast<size_t>(v.num_vars), m = static_cast<size_t>(v.num_cons);
+  for (size_t j = 0; j < n; ++j)
+    if (!std::isfinite(v.objective[j]))
+      throw InvalidProblemError("objective coefficient " + std::to_string(j) + " is not finite");
+  if (!std::isfinite(v.objective_offset)) throw InvalidProblemError("objective offset is not finite");
+  check_bounds(std::span<const double>(v.var_lb, n), std::span<const double>(v.var_ub, n), "variable");
+  check_bounds(std::span<const double>(v.con_lb, m), std::span<const double>(v.con_ub, m), "constraint");
+}
+
 bool operator==(const LpProblem& a, const LpProblem& b) {
   return a.name == b.name && a.objective == b.objective &&
          a.objective_offset == b.objective_offset && a.matrix == b.matrix &&

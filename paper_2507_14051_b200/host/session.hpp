@@ -4,6 +4,7 @@
 
 #include <chrono>
 #include <memory>
+#include <string>
 
 #include "device.hpp"
 #include "kkt.hpp"
@@ -20,6 +21,10 @@ using Clock = std::chrono::steady_clock;
 class Session {
  public:
   Session(const LpProblem& problem, const SolverConfig& cfg, const DeviceOptions& dopt);
+  // Zero-copy: the view's arrays are borrowed and must outlive the session.
+  // The matrix is validated by the device ingest (same exception classes and
+  // messages as SparseMatrix::from_csr), the vectors as LpProblem::validate.
+  Session(const rhpdhg_lp_view& view, const SolverConfig& cfg, const DeviceOptions& dopt);
   ~Session();
   bool step();                   // false once decided
   bool advance(long iterations); // runs blocks until >= iterations more are done or decided
@@ -34,9 +39,12 @@ class Session {
   rhp_ctx* device() const;
 
  private:
+  Session(const rhpdhg_lp_view& view, const std::string& name, bool validated,
+          const SolverConfig& cfg, const DeviceOptions& dopt);
   KktResiduals kkt_check(int which);
 
-  const LpProblem& problem_;
+  rhpdhg_lp_view view_{};  // the problem's arrays (borrowed)
+  std::string name_;
   SolverConfig cfg_;
   std::unique_ptr<detail::Device> dev_;
   Clock::time_point t0_, t_loop_;

@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #include "device.hpp"
@@ -119,19 +120,54 @@ SolutionReport solve(const LpProblem& problem, const SolverConfig& cfg) {
 // solve() as a resumable state machine so callers (bench, FFI) can advance
 // the loop in slices; solve() runs it to completion.
 Session::Session(const LpProblem& problem, const SolverConfig& cfg, const DeviceOptions& dopt)
-    : problem_(problem), cfg_(cfg) {
+    : Session((cfg.validate(), problem.validate(), detail::view_of(problem)), problem.name, true, cfg,
+              dopt) {}
+
+Session::Session(const rhpdhg_lp_view& view, const SolverConfig& cfg, const DeviceOptions& dopt)
+    : Session(view, std::string(), false, cfg, dopt) {}
+
+Session::Session(const rhpdhg_lp_view& view, const std::string& name, bool validated,
+                 const SolverConfig& cfg, const DeviceOptions& dopt)
+    : view_(view), name_(name), cfg_(cfg) {
   cfg.validate();
-  problem.validate();
   t0_ = Clock::now();
-  const Index n = problem.num_vars();
-  dev_ = std::make_unique<detail::Device>(detail::view_of(problem), detail::options(dopt));
+  // RHPDHG_SETUP_TRACE=1: per-phase setup times on stderr
+  const bool trace = std::getenv("RHPDHG_SETUP_TRACE") != nullptr;
+  Clock::time_point tp = t0_;
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    const Clock::time_point now = Clock::now();
+    std::fprintf(stderr, "setup %-24s %9.3f s\n", what, std::chrono::duration<double>(now - tp).count());
+    tp = now;
+  };
+  const Index n = view.num_vars;
+  if (view.num_cons < 0 || view.num_vars < 0) throw UsageError("matrix dimensions must be nonnegative");
+  // the matrix is validated by the device ingest (from_csr's exceptions),
+  // then the vectors (LpProblem::validate, lp_problem.cpp:30-46)
+  dev_ = std::make_unique<detail::Device>(view, detail::options(dopt));
   rhp_ctx* c = dev_->get();
+  if (!validated) detail::validate_vectors(view);
+  // nonzeros after the ingest dropped explicit zeros (SparseMatrix::nnz())
+  Index nnz = view.nnz;
+  if (!validated) {
+    rhp_layout_info li{};
+    detail::ok(rhp_layout(c, &li), "rhp_layout");
+    nnz = li.nnz_local;
+    if (dopt.world_size > 1) {  // local count on this rank: count the global one on the host
+      nnz = 0;
+      if (view.num_cons > 0)
+        for (Index e = view.row_ptr[0]; e < view.row_ptr[view.num_cons]; ++e) nnz += view.values[e] != 0.0;
+    }
+  }
+  phase("device create+ingest");
   // (1) diagonal preconditioning on the device (solver.cpp:72-78)
   detail::ok(rhp_scale(c, cfg.scaling_enabled ? 1 : 0, cfg.ruiz_iterations, cfg.pock_chambolle ? 1 : 0),
              "rhp_scale");
+  phase("scaling");
   // (2) step size from the scaled norm (solver.cpp:81-88)
   const PowerIterationResult pi = device_power_iteration(
-      c, n, problem.matrix.nnz(), cfg.power_tol, cfg.power_max_iters, cfg.power_seed);
+      c, n, nnz, cfg.power_tol, cfg.power_max_iters, cfg.power_seed);
+  phase("power iteration");
   step_.matrix_norm_estimate = pi.value;
   step_.step_size = default_stepsize(pi.value, cfg.stepsize_multiplier);
   step_.primal_weight = cfg.initial_weight;
@@ -144,9 +180,8 @@ Session::Session(const LpProblem& problem, const SolverConfig& cfg, const Device
   spmv_counter::add(report_.spmv_setup);
   if (cfg.verbosity >= 1)
     std::fprintf(stderr, "%s: %ld rows, %ld cols, %ld nonzeros, ||A|| ~ %.6e, eta %.6e\n",
-                 problem.name.empty() ? "instance" : problem.name.c_str(),
-                 static_cast<long>(problem.num_cons()), static_cast<long>(n),
-                 static_cast<long>(problem.matrix.nnz()), pi.value, step_.step_size);
+                 name_.empty() ? "instance" : name_.c_str(), static_cast<long>(view.num_cons),
+                 static_cast<long>(n), static_cast<long>(nnz), pi.value, step_.step_size);
   // (3) zero start, anchor = snapshot = start (solver.cpp:91-103)
   const rhp_step dstep = device_step(step_, cfg);
   detail::ok(rhp_set_step(c, &dstep), "rhp_set_step");
@@ -155,9 +190,10 @@ Session::Session(const LpProblem& problem, const SolverConfig& cfg, const Device
   pid_.ki = cfg.pid_ki;
   pid_.kd = cfg.pid_kd;
   pid_.omega = cfg.initial_weight;
-  denoms_ = detail::problem_denoms(problem);
+  denoms_ = detail::problem_denoms(view);
   tol_.epsilon = cfg.epsilon;
   report_.setup_seconds = since(t0_);
+  phase("step/iterate/denoms");
   t_loop_ = Clock::now();
   // initial check: the zero start may already be optimal (solver.cpp:136-145)
   last_ = kkt_check(0);
@@ -248,16 +284,16 @@ SolutionReport Session::finish() {
   rhp_ctx* c = dev_->get();
   if (status_ != SolveStatus::optimal) last_ = kkt_check(0);
   report_.loop_seconds = since(t_loop_);
-  const Index m = problem_.num_cons(), n = problem_.num_vars();
+  const Index m = view_.num_cons, n = view_.num_vars;
   report_.status = status_;
   report_.x.resize(static_cast<size_t>(n));
   report_.y.resize(static_cast<size_t>(m));
   report_.reduced_costs.resize(static_cast<size_t>(n));
   detail::ok(rhp_fetch_solution(c, report_.x.data(), report_.y.data(), report_.reduced_costs.data()),
              "rhp_fetch_solution");
-  double acc = problem_.objective_offset;  // solver.cpp:211-218
-  for (size_t j = 0; j < report_.x.size(); ++j) acc += problem_.objective[j] * report_.x[j];
-  report_.objective = problem_.maximization ? -acc : acc;
+  double acc = view_.objective_offset;  // solver.cpp:211-218
+  for (size_t j = 0; j < report_.x.size(); ++j) acc += view_.objective[j] * report_.x[j];
+  report_.objective = view_.maximization ? -acc : acc;
   report_.residuals = last_;
   report_.iterations = total_;
   report_.restart_count = restarts_;

@@ -39,6 +39,17 @@ Denoms problem_denoms(const LpProblem& p) {
   return Denoms{1.0 + std::sqrt(bound2), 1.0 + std::sqrt(c2)};
 }
 
+Denoms problem_denoms(const rhpdhg_lp_view& v) {
+  double bound2 = 0.0;
+  for (int64_t i = 0; i < v.num_cons; ++i) {
+    if (std::isfinite(v.con_lb[i])) bound2 += v.con_lb[i] * v.con_lb[i];
+    if (std::isfinite(v.con_ub[i])) bound2 += v.con_ub[i] * v.con_ub[i];
+  }
+  double c2 = 0.0;
+  for (int64_t j = 0; j < v.num_vars; ++j) c2 += v.objective[j] * v.objective[j];
+  return Denoms{1.0 + std::sqrt(bound2), 1.0 + std::sqrt(c2)};
+}
+
 KktResiduals residuals_from_sums(const rhp_kkt_sums& s, const Denoms& d) {
   if (s.nan_x > 0) throw NumericalBreakdownError("NaN in primal iterate");
   if (s.nan_y > 0) throw NumericalBreakdownError("NaN in dual iterate");

@@ -310,6 +310,7 @@ def run_product(args):
     iters_all = iters
 
     # ---- live kernel timing for the roofline (after the timed region)
+    gc = sess.gather_ceiling(reps=5)
     kt = sess.time_kernels(reps=20)
     sess.close()
     # per-GPU algorithmic bytes (local rows / nonzeros on the partitioned path)
@@ -331,14 +332,22 @@ def run_product(args):
                 if traffic else None,
                 "kernel": ("spmv_fused<EpiAty> (A^T y+ + aty Halpern + next primal step)"
                            if dominant == "k2" else
-                           "spmv_fused<EpiDual> (A x+ + dual step + Halpern/reflection)"),
+                           "spmv_fused<EpiDual> (A x+ + dual step + Halpern/reflection)")
+                + (" [thread-per-row engine]" if layout.get("thread_rows", {}).get(
+                    "At" if dominant == "k2" else "A") else " [merge-path engine]"),
                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "bytes_per_launch": k2b if dominant == "k2" else k1b,
                 "kernels": {"k1_ms": kt["k1_dual_spmv_ms"], "k1_gbs": k1,
                             "k2_ms": kt["k2_aty_spmv_primal_ms"], "k2_gbs": k2,
                             "k3_ms": kt["k3_primal_ms"],
                             "iteration_bytes": iter_bytes,
-                            "iteration_gbs_in_loop": iter_bytes * value / 1e9}}
+                            "iteration_gbs_in_loop": iter_bytes * value / 1e9},
+                # the non-HBM ceiling: a probe kernel doing only the SpMV's
+                # irreducible index/value stream + 8-B gathers + FMA on the
+                # same operator (rhp_gather_ceiling); frac = probe / kernel
+                "gather_ceiling": {"a_ms": gc["A"], "at_ms": gc["At"],
+                                   "k1_frac": gc["A"] / kt["k1_dual_spmv_ms"],
+                                   "k2_frac": gc["At"] / kt["k2_aty_spmv_primal_ms"]}}
 
     # ---- e2e through the C ABI with host buffers, to 1e-8 (cap)
     e2e = None
@@ -367,7 +376,8 @@ def run_product(args):
                "status": rep.status, "iterations": rep.iterations, "restarts": rep.restart_count,
                "time_to_tol_s": t_e2e, "tol": args.e2e_eps,
                "time_to_1e-4_s": t_1e4, "iterations_to_1e-4": it_1e4 if t_1e4 else None,
-               "setup_s": t_setup, "objective": rep.objective,
+               "setup_s": t_setup, "power_iterations": rep.power_iterations,
+               "objective": rep.objective,
                "residuals": vars(rep.residuals)}
 
     cpu = None

@@ -194,6 +194,9 @@ int rhpdhg_session_timer(rhpdhg_session* s, int start, double* ms);
  * `reps` launches (rhp_time_kernels); mutates the iterate, so call it only
  * after the measured work. ms3 = {K1, K2, K3}. */
 int rhpdhg_session_time_kernels(rhpdhg_session* s, int reps, double* ms3);
+/* Benchmark hook: gather ceilings of A and A^T (rhp_gather_ceiling), ms2 =
+ * {A, A^T}. */
+int rhpdhg_session_gather_ceiling(rhpdhg_session* s, int reps, double* ms2);
 /* Device layout summary: m, n, nnz, then rows of A and of A^T per schedule
  * bin (8 each), the grids of the A, A^T and vector kernels, the SM count,
  * the gather cache policy (bit 0: A through L1, bit 1: A^T) and whether the

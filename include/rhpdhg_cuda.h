@@ -203,6 +203,11 @@ int rhp_time_kernels(rhp_ctx* ctx, int reps, double* ms_k1, double* ms_k2, doubl
 /* Average device ms of `reps` plain SpMVs (transpose 0: A v, 1: A^T v) on
  * the current matrix, no epilogue: the SpMV engine's own rate. */
 int rhp_time_spmv(rhp_ctx* ctx, int transpose, int reps, double* ms);
+/* Gather ceiling (diagnostic): best device ms over `reps` of a kernel doing
+ * only the irreducible SpMV work on A's / A^T's own nonzeros (coalesced index
+ * + value stream, 8-B gathers with the operator's cache policy, one FMA
+ * each). Either output may be null. */
+int rhp_gather_ceiling(rhp_ctx* ctx, int reps, double* ms_a, double* ms_at);
 /* cudaProfilerStart (start != 0) / cudaProfilerStop: brackets the launches
  * an `ncu --profile-from-start off` capture should see. */
 int rhp_profiler_range(int start);

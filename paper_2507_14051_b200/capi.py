@@ -190,7 +190,7 @@ CUDA_SYMBOLS = [
     "rhp_reset_iterate", "rhp_set_iterate", "rhp_run_block", "rhp_get_history", "rhp_kkt",
     "rhp_kkt_of", "rhp_fetch_solution", "rhp_fetch_iterate", "rhp_restart", "rhp_any",
     "rhp_partition_rows",
-    "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_time_spmv", "rhp_profiler_range",
+    "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_time_spmv", "rhp_gather_ceiling", "rhp_profiler_range",
     "rhp_synchronize",
 ]
 HOST_SYMBOLS = [
@@ -200,6 +200,7 @@ HOST_SYMBOLS = [
     "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
+    "rhpdhg_session_gather_ceiling",
     "rhpdhg_session_layout", "rhpdhg_lp_read_mps", "rhpdhg_lp_view_of", "rhpdhg_lp_free",
 ]
 
@@ -253,6 +254,7 @@ def load_cuda() -> C.CDLL:
             "rhp_time_kernels": [P, C.c_int, c_double_p, c_double_p, c_double_p],
             "rhp_profiler_range": [C.c_int],
             "rhp_time_spmv": [P, C.c_int, C.c_int, c_double_p],
+            "rhp_gather_ceiling": [P, C.c_int, c_double_p, c_double_p],
             "rhp_synchronize": [P],
         }
         for name, args in sig.items():
@@ -290,6 +292,7 @@ def load_host() -> C.CDLL:
                                     c_int64_p, c_int64_p],
             "rhpdhg_session_timer": [P, C.c_int, c_double_p],
             "rhpdhg_session_time_kernels": [P, C.c_int, c_double_p],
+            "rhpdhg_session_gather_ceiling": [P, C.c_int, c_double_p],
             "rhpdhg_session_layout": [P, c_int64_p],
             "rhpdhg_session_finish": [P, C.POINTER(ReportC), c_double_p, c_double_p, c_double_p,
                                       c_double_p, C.c_int64],

@@ -72,6 +72,14 @@ __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((
 #endif
 template <bool L1G = false>
 __device__ __forceinline__ double ld_gather(const double* p) {
+#ifdef RHP_GATHER_EVICT_LAST  // experiment: keep gathered lines in L2 ahead of everything else
+  double e;
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  if constexpr (L1G) asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(e) : "l"(p), "l"(pol));
+  else asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(e) : "l"(p), "l"(pol));
+  return e;
+#else
   if constexpr (L1G) return __ldg(p);  // L1-allocating: small or clustered vectors
 #if RHP_GATHER_MODE == 1
   return __ldcg(p);  // L2 only
@@ -81,6 +89,7 @@ __device__ __forceinline__ double ld_gather(const double* p) {
   return v;
 #else
   return __ldg(p);  // read-only path
+#endif
 #endif
 }
 

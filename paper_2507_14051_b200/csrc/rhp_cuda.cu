@@ -15,6 +15,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #ifdef RHP_WITH_NCCL
@@ -316,6 +317,37 @@ EpiStore store_into(double* out) {
   EpiStore e{};
   e.out = out;
   return e;
+}
+
+// Gather-ceiling probe: the irreducible work of one SpMV over an operator's
+// own nonzeros — stream its column indices and values coalesced, gather
+// x[col] (8-B loads through the operator's cache policy), one FMA each — at
+// full occupancy, with no rows, scans or epilogue. No SpMV over that operator
+// can beat it, so bench.py reports K1/K2 against it next to the HBM roofline.
+template <bool L1G>
+__global__ void __launch_bounds__(256) k_gather_probe(const int32_t* __restrict__ ci,
+                                                      const double* __restrict__ v,
+                                                      const double* __restrict__ x, int64_t nnz,
+                                                      double* out) {
+  constexpr int U = 4;
+  double s = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * U;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x * U + threadIdx.x; b < nnz; b += stride) {
+    int c[U];
+    double w[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t i = b + static_cast<int64_t>(k) * blockDim.x;
+      c[k] = i < nnz ? __ldcs(ci + i) : 0;
+      w[k] = i < nnz ? __ldcs(v + i) : 0.0;
+    }
+    double g[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) g[k] = ld_gather<L1G>(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < U; ++k) s = fma(w[k], g[k], s);
+  }
+  out[static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x] = s;
 }
 
 // SpMV engine per operator (deterministic, from the row lengths only, so two
@@ -1339,6 +1371,40 @@ int rhp_time_kernels(rhp_ctx* c, int reps, double* ms_k1, double* ms_k2, double*
 
 // Average device ms of `reps` plain SpMVs (out = A v or A^T v, no epilogue
 // reductions) on the current matrix: the SpMV engine's own rate.
+int rhp_gather_ceiling(rhp_ctx* c, int reps, double* ms_a, double* ms_at) {
+  return guarded([&] {
+    cudaStream_t s = c->stream;
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, reinterpret_cast<const void*>(k_gather_probe<false>), 256, 0));
+    const int grid = c->sm_count * std::max(occ, 1);
+    double* out = nullptr;
+    CK(cudaMalloc(&out, static_cast<size_t>(grid) * 256 * sizeof(double)));
+    auto run = [&](const DevOp& op, const double* x) {
+      if (op.l1g) k_gather_probe<true><<<grid, 256, 0, s>>>(op.ci, op.v, x, op.nnz, out);
+      else k_gather_probe<false><<<grid, 256, 0, s>>>(op.ci, op.v, x, op.nnz, out);
+    };
+    for (auto [op, x, ms] : {std::tuple<const DevOp*, const double*, double*>{&c->A, c->xp, ms_a},
+                             {&c->At, c->yp, ms_at}}) {
+      if (!ms) continue;
+      run(*op, x);  // warm-up
+      float best = 1e30f;
+      for (int r = 0; r < std::max(reps, 1); ++r) {
+        CK(cudaEventRecord(c->tev0, s));
+        run(*op, x);
+        CK(cudaEventRecord(c->tev1, s));
+        CK(cudaEventSynchronize(c->tev1));
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+        best = std::min(best, f);
+      }
+      *ms = best;
+    }
+    CK(cudaGetLastError());
+    CK(cudaFree(out));
+  });
+}
+
 int rhp_time_spmv(rhp_ctx* c, int transpose, int reps, double* ms) {
   return guarded([&] {
     cudaStream_t s = c->stream;

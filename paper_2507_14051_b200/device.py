@@ -58,7 +58,10 @@ class DeviceContext:
         return {"m_local": info.m_local, "n": info.n, "nnz_local": info.nnz_local,
                 "row_bins": list(info.row_bins), "col_bins": list(info.col_bins),
                 "grid_a": info.grid_a, "grid_at": info.grid_at, "grid_vec": info.grid_vec,
-                "sm_count": info.sm_count}
+                "sm_count": info.sm_count,
+                "gather_l1": {"A": bool(info.gather_l1 & 1), "At": bool(info.gather_l1 & 2)},
+                "pdl": bool(info.pdl),
+                "thread_rows": {"A": bool(info.thread_rows & 1), "At": bool(info.thread_rows & 2)}}
 
     def scale(self, enabled=True, ruiz=10, pock_chambolle=True):
         self._ok(self.lib.rhp_scale(self.h, int(enabled), ruiz, int(pock_chambolle)))

@@ -258,6 +258,12 @@ int rhpdhg_session_time_kernels(rhpdhg_session* s, int reps, double* ms3) {
   });
 }
 
+int rhpdhg_session_gather_ceiling(rhpdhg_session* s, int reps, double* ms2) {
+  return guarded([&] {
+    detail::ok(rhp_gather_ceiling(s->session->device(), reps, &ms2[0], &ms2[1]), "rhp_gather_ceiling");
+  });
+}
+
 int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
   return guarded([&] {
     rhp_layout_info li{};

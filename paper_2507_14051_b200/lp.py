@@ -453,6 +453,12 @@ class Session:
         self._check(self._lib.rhpdhg_session_time_kernels(self._h, reps, ms))
         return {"k1_dual_spmv_ms": ms[0], "k2_aty_spmv_primal_ms": ms[1], "k3_primal_ms": ms[2]}
 
+    def gather_ceiling(self, reps: int = 5) -> dict:
+        """Best device ms of the pure-gather probe over A and A^T."""
+        ms = (C.c_double * 2)()
+        self._check(self._lib.rhpdhg_session_gather_ceiling(self._h, reps, ms))
+        return {"A": ms[0], "At": ms[1]}
+
     def layout(self) -> dict:
         o = (C.c_int64 * 27)()
         self._check(self._lib.rhpdhg_session_layout(self._h, o))

@@ -223,6 +223,51 @@ def test_both_block_engines_match_oracle(gpu, mode):
         set_resident(-1)
 
 
+ENGINE_LPS = [c3_transport(S=40, T=70), c1_small(m=300, n=500), ragged_lp()]
+
+
+@pytest.mark.parametrize("lp", ENGINE_LPS, ids=[c.name for c in ENGINE_LPS])
+def test_spmv_engines_and_gather_policies(gpu, lp, monkeypatch):
+    """Both SpMV engines (merge-path warps; thread per row, chosen for
+    operators whose rows all have <= 8 nonzeros) under both gather cache
+    policies: SpMV within 1e-14 of the oracle (bit-exact for the
+    thread-per-row engine, which sums in the reference's order), solves that
+    match the reference, and gather policies that never change a result."""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, lp.num_vars)
+    y = rng.uniform(-1, 1, lp.num_cons)
+    O = support.oracle()
+    ref_ax, ref_aty = support.spmv_with(O, lp, x), support.spmv_with(O, lp, y, True)
+    cfg = SolverConfig(epsilon=1e-8)
+    o = support.solve_with(O, lp, cfg)
+    longest_t = int(np.max(np.bincount(lp.col_index, minlength=lp.num_vars))) if lp.nnz else 0
+    for rows in ("0", "1"):
+        results = []
+        for l1 in ("0", "1"):
+            monkeypatch.setenv("RHP_THREAD_ROWS", rows)
+            monkeypatch.setenv("RHP_L1_GATHER", l1)
+            with DeviceContext(lp) as dev:
+                lay = dev.layout()
+                ax, aty = dev.spmv(x), dev.spmv(y, True)
+            assert lay["gather_l1"] == {"A": l1 == "1", "At": l1 == "1"}
+            assert lay["thread_rows"]["At"] == (rows == "1" and longest_t <= 64)
+            for got, ref, row_engine in ((ax, ref_ax, lay["thread_rows"]["A"]),
+                                         (aty, ref_aty, lay["thread_rows"]["At"])):
+                if row_engine:
+                    assert np.array_equal(got, ref)
+                else:
+                    assert max_rel(got, ref) <= 1e-13
+            g = solve(lp, cfg)
+            assert g.status == o.status == "optimal"
+            assert abs(g.objective - o.objective) <= 1e-6 * max(1.0, abs(o.objective))
+            g30 = solve(lp, SolverConfig(epsilon=1e-300, iteration_limit=30))
+            o30 = support.solve_with(O, lp, SolverConfig(epsilon=1e-300, iteration_limit=30))
+            assert max_rel(g30.x, o30.x) <= 1e-10 and max_rel(g30.y, o30.y) <= 1e-10
+            results.append(g)
+        a, b = results
+        assert a.iterations == b.iterations and np.array_equal(a.x, b.x) and np.array_equal(a.y, b.y)
+
+
 def test_operator_budget_and_counters(gpu):
     lp = support.lp_from_json(RANDOM[1]["lp"])
     r = solve(lp, SolverConfig(epsilon=1e-6))

@@ -11,7 +11,7 @@ mkdir -p "$OUT"
 # plain launches: ncu cannot profile kernel nodes of graphs with conditional nodes
 BENCH="python bench.py --config $CFG --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-graph"
 # 1) launch list with per-launch device time (cold-cache, serialised), past setup
-ncu --metrics gpu__time_duration.sum --clock-control none -s 700 -c 300 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -s ${SKIP:-700} -c 300 --csv \
     --log-file "$OUT/launches_${TAG}_${CFG}.csv" $BENCH > /dev/null
 # 2) full sections of K3 / K1 / K2 on a live iterate: bench.py --profile-kernels
 #    brackets exactly 2 launches of each with cudaProfilerStart/Stop

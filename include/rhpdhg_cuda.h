@@ -133,8 +133,8 @@ typedef struct rhp_layout_info {
   int32_t sm_count;
   int32_t gather_l1;    /* bit 0: A's SpMV gathers through L1, bit 1: A^T's (tuned at create) */
   int32_t pdl;          /* SpMVs use programmatic dependent launch */
-  int32_t thread_rows;  /* bit 0: A uses the thread-per-row engine, bit 1: A^T */
-  int32_t pad_;
+  int32_t thread_rows;  /* bit 0: A uses the thread-per-row engine, bit 1: A^T (last segment) */
+  int32_t segments;     /* column segments: A's in bits 0-15, A^T's in bits 16-31 (1 = unsegmented) */
 } rhp_layout_info;
 
 const char* rhp_last_error(void);

@@ -193,6 +193,8 @@ struct Sched {
   double* slot_part;          // [2 * n_chunks] per chunk: head partial, tail partial
   unsigned int* slot_ticket;  // [n_multi]
   double* long_red;           // [n_multi * 16] epilogue reductions of split rows
+  const double* seg_in;       // column-segmented operators (segments.cuh): running row sums of the
+                              // previous segments, added to every row sum before its epilogue; else null
 };
 
 struct Csr {

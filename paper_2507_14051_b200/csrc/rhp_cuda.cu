@@ -28,6 +28,7 @@
 #include "pdhg_kernels.cuh"
 #include "resident.cuh"
 #include "scaling_kernels.cuh"
+#include "segments.cuh"
 #include "rhpdhg_cuda.h"
 
 using namespace rhp;
@@ -117,6 +118,11 @@ struct DevOp : DeviceCsr {
   double *slot_part = nullptr, *long_red = nullptr;
   unsigned int* slot_ticket = nullptr;
   bool l1g = false;  // L1-allocating gathers (tune_gathers)
+  // column segments (segments.cuh, build_segments): when non-empty the SpMV
+  // walks segs[0..S-1] in order, the last one with the real epilogue, and
+  // every schedule-dependent use goes through fin() (the last segment)
+  std::vector<DevOp> segs;
+  double* segbuf = nullptr;  // [rows] running row sums of the segments
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
 
@@ -216,13 +222,19 @@ void upload_sched(DevOp& d, const HostOperator& h, cudaStream_t s) {
 }
 
 void free_op(DevOp& d) {
+  for (DevOp& g : d.segs) free_op(g);
   for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.warp_row,
                   (void*)d.warp_nz, (void*)d.slot_row, (void*)d.head_slot, (void*)d.tail_slot,
                   (void*)d.slot_first, (void*)d.slot_count, (void*)d.slot_part,
-                  (void*)d.long_red, (void*)d.slot_ticket})
+                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.segbuf})
     if (p) cudaFree(p);
   d = DevOp{};
 }
+
+// The operator whose schedule carries the fused epilogue: the last column
+// segment of a segmented operator, else the operator itself. K3 and the
+// partitioned walkers walk its schedule and K1's finalize reads its slots.
+const DevOp& fin(const DevOp& op) { return op.segs.empty() ? op : op.segs.back(); }
 
 // First index of a contiguous ascending permutation (the layout keeps rows
 // and columns in their original order, so every map is one), else -1.
@@ -283,8 +295,8 @@ int vec_grid(const rhp_ctx& c, int64_t len) {
 // gains nothing on C2 (6904 vs 6895 iter/s) and loses 6% on C3 (20.1k vs
 // 18.9k) — the graph already launches the next kernel back to back.
 template <class Epi>
-void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
-                 double* part, unsigned int* ticket, cudaStream_t s) {
+void launch_one(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
+                double* part, unsigned int* ticket, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kBlock);
@@ -296,6 +308,23 @@ void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const 
   cfg.numAttrs = c.pdl ? 1 : 0;
   if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
   else CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
+}
+
+EpiStore store_into(double* out);
+
+// One SpMV with its fused epilogue; a column-segmented operator runs its
+// segments in order (each adds its row sums to segbuf), the last one with
+// the epilogue.
+template <class Epi>
+void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const Epi& epi,
+                 double* part, unsigned int* ticket, cudaStream_t s) {
+  if (op.segs.empty()) {
+    launch_one(c, op, grid, xg, epi, part, ticket, s);
+    return;
+  }
+  for (size_t k = 0; k + 1 < op.segs.size(); ++k)
+    launch_one(c, op.segs[k], grid, xg, store_into(op.segbuf), nullptr, nullptr, s);
+  launch_one(c, op.segs.back(), grid, xg, epi, part, ticket, s);
 }
 
 // Resident CTAs per SM of an SpMV instantiation.
@@ -354,16 +383,111 @@ __global__ void __launch_bounds__(256) k_gather_probe(const int32_t* __restrict_
 // contexts on one LP always agree bit for bit): thread-per-row when the
 // longest row has <= kThreadRowMax nonzeros, else the merge-path warp engine.
 // RHP_THREAD_ROWS=0 forces merge path; =1 allows rows up to 64 nonzeros.
-void choose_engines(rhp_ctx& c) {
+void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
   const char* env = std::getenv("RHP_THREAD_ROWS");
   const int64_t cap = env && env[0] == '0' ? -1 : env && env[0] == '1' ? 64 : kThreadRowMax;
-  for (auto [d, h] : {std::pair<DevOp*, const HostOperator*>{&c.A, &c.L.A}, {&c.At, &c.L.At}}) {
-    int64_t longest = 0;
-    for (int64_t r = 0; r < h->rows; ++r) longest = std::max(longest, h->rp[r + 1] - h->rp[r]);
-    if (h->rows > 0 && longest <= cap) {
-      d->sched.thread_rows = 1;
-      d->sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
-    }
+  const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
+  int64_t longest = 0;
+  for (int64_t r = 0; r < rows; ++r) longest = std::max(longest, rp[r + 1] - rp[r]);
+  if (rows > 0 && longest <= cap) {
+    d.sched.thread_rows = 1;
+    d.sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
+  }
+}
+
+void choose_engines(rhp_ctx& c) {
+  apply_engine_rule(c.A, c.L.A.rp);
+  apply_engine_rule(c.At, c.L.At.rp);
+}
+
+__global__ void k_mark_sectors(const int32_t* ci, int64_t lo, int64_t hi, unsigned int* bits) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = lo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < hi; e += stride) {
+    const uint32_t sector = static_cast<uint32_t>(ci[e]) >> 2;  // 4 doubles per 32-B sector
+    atomicOr(bits + (sector >> 5), 1u << (sector & 31));
+  }
+}
+
+__global__ void k_popcount(const unsigned int* bits, int64_t words, unsigned long long* total) {
+  unsigned long long t = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride)
+    t += __popc(bits[i]);
+  if (t) atomicAdd(total, t);
+}
+
+// Gather footprint of the interleaved schedule (layout.cu: the grid walks
+// one band of W consecutive chunks at a time): the distinct 32-B sectors of
+// the gathered vector touched by a band, times 32 B, maximised over up to 8
+// bands spread over the operator. Deterministic (structure only).
+double band_footprint_bytes(rhp_ctx& c, const DevOp& d, const HostOperator& h, int64_t cols) {
+  const int64_t W = h.sched.n_warps, chunks = h.sched.n_chunks;
+  if (W <= 0 || chunks <= W) return static_cast<double>(cols) * 8.0;  // one band: the whole operator
+  const int64_t bands = chunks / W;
+  const int64_t words = (cols / 4) / 32 + 2;
+  unsigned int* bits = dev_alloc<unsigned int>(static_cast<size_t>(words));
+  unsigned long long* total = dev_alloc<unsigned long long>(1);
+  double worst = 0.0;
+  const int64_t samples = std::min<int64_t>(8, bands);
+  for (int64_t k = 0; k < samples; ++k) {
+    const int64_t b = bands * k / samples;
+    const int64_t lo = h.warp_nz[b * W], hi = h.warp_nz[std::min(chunks, (b + 1) * W)];
+    CK(cudaMemsetAsync(bits, 0, words * sizeof(unsigned int), c.stream));
+    CK(cudaMemsetAsync(total, 0, sizeof(unsigned long long), c.stream));
+    if (hi > lo) k_mark_sectors<<<c.sm_count * 4, 256, 0, c.stream>>>(d.ci, lo, hi, bits);
+    k_popcount<<<c.sm_count * 4, 256, 0, c.stream>>>(bits, words, total);
+    unsigned long long t = 0;
+    CK(cudaMemcpyAsync(&t, total, sizeof(t), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    worst = std::max(worst, 32.0 * static_cast<double>(t));
+  }
+  cudaFree(bits);
+  cudaFree(total);
+  return worst;
+}
+
+// Column segments (segments.cuh) of an operator whose gathered vector is
+// larger than RHP_SEG_BYTES (default 48 MB, 0 disables) AND whose
+// interleaved bands still gather from more than that (C5's random columns:
+// yes; C4's commodity-ordered columns: no — there segments only add row
+// passes, K1 0.39 -> 0.61 ms). RHP_SEG_FORCE=1 skips the band test (tests).
+// Equal column ranges, each with its own merge-path schedule for the
+// operator's grid and its own engine choice; the cache policy is the
+// operator's. Built after scaling (the values are final), rebuilt if scaling
+// runs again. A pure function of the structure, so it never makes two
+// contexts on one LP differ.
+void build_segments(rhp_ctx& c, DevOp& d, const HostOperator& h, int64_t cols, int grid) {
+  for (DevOp& g : d.segs) free_op(g);
+  d.segs.clear();
+  if (d.segbuf) cudaFree(d.segbuf);
+  d.segbuf = nullptr;
+  double seg_bytes = 48.0 * 1024 * 1024;
+  if (const char* e = std::getenv("RHP_SEG_BYTES")) seg_bytes = std::atof(e);
+  if (!(seg_bytes > 0) || d.nnz == 0) return;
+  const int64_t S = static_cast<int64_t>(std::ceil(static_cast<double>(cols) * 8.0 / seg_bytes));
+  if (S <= 1) return;
+  const char* force = std::getenv("RHP_SEG_FORCE");
+  if (!(force && force[0] == '1') && band_footprint_bytes(c, d, h, cols) <= seg_bytes) return;
+  std::vector<int32_t> cb(static_cast<size_t>(S) + 1);
+  for (int64_t k = 0; k <= S; ++k) cb[k] = static_cast<int32_t>(cols * k / S);
+  std::vector<DeviceCsr> parts;
+  std::vector<std::vector<int64_t>> hrp;
+  split_columns(d, cb, parts, hrp, c.stream);
+  d.segbuf = dev_alloc<double>(static_cast<size_t>(d.rows));
+  d.segs.resize(static_cast<size_t>(S));
+  for (int64_t k = 0; k < S; ++k) {
+    DevOp& g = d.segs[k];
+    static_cast<DeviceCsr&>(g) = parts[k];
+    HostOperator h;
+    h.rows = d.rows;
+    h.cols = cb[k + 1] - cb[k];
+    h.nnz = parts[k].nnz;
+    h.rp = std::move(hrp[k]);
+    build_schedule(h, static_cast<int64_t>(grid) * kWarps, kRowWeight);
+    upload_sched(g, h, c.stream);
+    apply_engine_rule(g, h.rp);
+    g.l1g = d.l1g;
+    g.sched.seg_in = k == 0 ? nullptr : d.segbuf;
   }
 }
 
@@ -411,8 +535,8 @@ EpiDual epi_dual(rhp_ctx& c, int token) {
   for (int k = 0; k < EpiDual::NIN; ++k) e.in[k] = in[k];
   e.part3 = c.part3;
   e.grid3 = c.grid_at;
-  e.n_multi3 = c.At.sched.n_multi;
-  e.long_red3 = c.At.long_red;
+  e.n_multi3 = fin(c.At).sched.n_multi;
+  e.long_red3 = fin(c.At).long_red;
   e.token = token;
   return e;
 }
@@ -467,8 +591,8 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   st.token = token;
   launch_spmv(c, c.At, c.grid_at, c.yp, st, nullptr, nullptr, s);
   allreduce(c, c.xchg, static_cast<size_t>(c.n) + 5, s);
-  k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, c.grid_at, c.At.sched.n_multi,
-                                      c.At.long_red, c.xchg + c.n, token);
+  k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, c.grid_at, fin(c.At).sched.n_multi,
+                                      fin(c.At).long_red, c.xchg + c.n, token);
   CK(cudaGetLastError());
   EpiAtyDist e{};
   e.ctl = c.ctl;
@@ -477,7 +601,7 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   const double* in[] = {c.xchg, c.aty, c.aty0, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiAtyDist::NIN; ++k) e.in[k] = in[k];
   e.token = token;
-  epilogue_walk<EpiAtyDist><<<c.grid_at, kBlock, 0, s>>>(c.At.sched, e, c.part3);
+  epilogue_walk<EpiAtyDist><<<c.grid_at, kBlock, 0, s>>>(fin(c.At).sched, e, c.part3);
   CK(cudaGetLastError());
 }
 
@@ -579,7 +703,7 @@ void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
   e.o = primal_out(c);
   const double* in[] = {c.aty, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiPrimal::NIN; ++k) e.in[k] = in[k];
-  epilogue_walk<EpiPrimal><<<c.grid_at, kBlock, 0, s>>>(c.At.sched, e, c.part3);
+  epilogue_walk<EpiPrimal><<<c.grid_at, kBlock, 0, s>>>(fin(c.At).sched, e, c.part3);
   CK(cudaGetLastError());
 }
 
@@ -661,8 +785,8 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
   ec.rcout = write_out ? c.rcout : nullptr;
   ec.part_row = c.partA;
   ec.grid_row = c.grid_a;
-  ec.n_multi_row = c.A.sched.n_multi;
-  ec.long_red_row = c.A.long_red;
+  ec.n_multi_row = fin(c.A).sched.n_multi;
+  ec.long_red_row = fin(c.A).long_red;
   if (!c.dist) {
     launch_spmv(c, c.At, c.grid_at, ys, ec, c.partAt, &c.ctl->ticket_kkt, c.stream);
   } else {
@@ -677,10 +801,10 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
     cd.col = ec;
     const double* in[] = {c.xchg, xs, c.cs, c.co, c.vlo, c.vuo};
     for (int k = 0; k < EpiKktColDist::NIN; ++k) cd.in[k] = in[k];
-    epilogue_walk<EpiKktColDist><<<c.grid_at, kBlock, 0, c.stream>>>(c.At.sched, cd, c.partAt);
+    epilogue_walk<EpiKktColDist><<<c.grid_at, kBlock, 0, c.stream>>>(fin(c.At).sched, cd, c.partAt);
     CK(cudaGetLastError());
     k_kkt_dist_finalize<<<1, kBlock, 0, c.stream>>>(c.ctl, c.partAt, c.grid_at,
-                                                    c.At.sched.n_multi, c.At.long_red,
+                                                    fin(c.At).sched.n_multi, fin(c.At).long_red,
                                                     c.xchg + c.n + 8);
     CK(cudaGetLastError());
   }
@@ -952,7 +1076,9 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->sm_count = c->sm_count;
     info->gather_l1 = (c->A.l1g ? 1 : 0) | (c->At.l1g ? 2 : 0);
     info->pdl = c->pdl ? 1 : 0;
-    info->thread_rows = (c->A.sched.thread_rows ? 1 : 0) | (c->At.sched.thread_rows ? 2 : 0);
+    info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0);
+    info->segments = static_cast<int32_t>(std::max<size_t>(1, c->A.segs.size()) |
+                                          (std::max<size_t>(1, c->At.segs.size()) << 16));
   });
 }
 
@@ -1016,6 +1142,16 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
     if (c->A.v_orig) CK(cudaFree(c->A.v_orig));
     if (c->At.v_orig) CK(cudaFree(c->At.v_orig));
     c->A.v_orig = c->At.v_orig = nullptr;
+    // column segments of the scaled operators (gathered vectors larger than L2)
+    build_segments(*c, c->A, c->L.A, c->n, c->grid_a);
+    build_segments(*c, c->At, c->L.At, c->m, c->grid_at);
+    if (c->graph_built) {  // the block graph captured the unsegmented launches
+      CK(cudaGraphExecDestroy(c->gexec));
+      CK(cudaGraphDestroy(c->graph));
+      c->gexec = nullptr;
+      c->graph = nullptr;
+      c->graph_built = false;
+    }
   });
 }
 
@@ -1058,9 +1194,9 @@ int rhp_power_step(rhp_ctx* c, double* vw, double* ww) {
       e.w = c->pw;
       e.in[0] = c->xchg;
       e.in[1] = c->pv;
-      epilogue_walk<EpiPowerDist><<<c->grid_at, kBlock, 0, c->stream>>>(c->At.sched, e, c->partAt);
+      epilogue_walk<EpiPowerDist><<<c->grid_at, kBlock, 0, c->stream>>>(fin(c->At).sched, e, c->partAt);
       k_power_dist_finalize<<<1, kBlock, 0, c->stream>>>(c->ctl, c->partAt, c->grid_at,
-                                                         c->At.sched.n_multi, c->At.long_red);
+                                                         fin(c->At).sched.n_multi, fin(c->At).long_red);
       CK(cudaGetLastError());
     }
     pull_ctl(*c);
@@ -1380,9 +1516,13 @@ int rhp_gather_ceiling(rhp_ctx* c, int reps, double* ms_a, double* ms_at) {
     const int grid = c->sm_count * std::max(occ, 1);
     double* out = nullptr;
     CK(cudaMalloc(&out, static_cast<size_t>(grid) * 256 * sizeof(double)));
-    auto run = [&](const DevOp& op, const double* x) {
+    auto run1 = [&](const DevOp& op, const double* x) {
       if (op.l1g) k_gather_probe<true><<<grid, 256, 0, s>>>(op.ci, op.v, x, op.nnz, out);
       else k_gather_probe<false><<<grid, 256, 0, s>>>(op.ci, op.v, x, op.nnz, out);
+    };
+    auto run = [&](const DevOp& op, const double* x) {  // segment by segment when segmented
+      if (op.segs.empty()) run1(op, x);
+      for (const DevOp& g : op.segs) run1(g, x);
     };
     for (auto [op, x, ms] : {std::tuple<const DevOp*, const double*, double*>{&c->A, c->xp, ms_a},
                              {&c->At, c->yp, ms_at}}) {

@@ -106,6 +106,7 @@ __device__ __forceinline__ void contribute(const Sched& s, Epi& epi, int slot, i
   double t = __ldcg(s.slot_part + 2 * first + 1);  // the first contributor's tail partial
   for (unsigned int k = 1; k < cnt; ++k) t += __ldcg(s.slot_part + 2 * (first + k));
   const int64_t row = s.slot_row[slot];
+  if (s.seg_in) t = add(__ldcg(s.seg_in + row), t);
   double ein[Epi::NIN > 0 ? Epi::NIN : 1];
   load_inputs(epi, row, ein);
   double la[Epi::NRED];
@@ -236,6 +237,9 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
             contribute(s, epi, hslot, 2 * static_cast<int64_t>(w), sum);
           }
         } else {
+          if constexpr (!WALK) {
+            if (s.seg_in) sum = add(__ldcg(s.seg_in + row), sum);
+          }
           load_inputs(epi, row, ein);
           epi.row(row, sum, ein, 1, acc);
         }
@@ -325,6 +329,12 @@ __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* val
           if (lo1 + t + u < hi1) s1 = add(s1, mul(v1[u], g1[u]));
           if (lo2 + t + u < hi2) s2 = add(s2, mul(v2[u], g2[u]));
         }
+      }
+    }
+    if constexpr (!WALK) {
+      if (s.seg_in) {
+        s1 = add(__ldcg(s.seg_in + i1), s1);
+        if (two) s2 = add(__ldcg(s.seg_in + i2), s2);
       }
     }
     epi.row(i1, s1, e1, 1, acc);

@@ -282,7 +282,7 @@ int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
     o[23] = li.gather_l1;
     o[24] = li.pdl;
     o[25] = li.thread_rows;
-    o[26] = 0;
+    o[26] = li.segments;
   });
 }
 

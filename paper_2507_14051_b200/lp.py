@@ -466,7 +466,8 @@ class Session:
                 "col_bins": list(o[11:19]), "grid_a": o[19], "grid_at": o[20],
                 "grid_vec": o[21], "sm_count": o[22],
                 "gather_l1": {"A": bool(o[23] & 1), "At": bool(o[23] & 2)}, "pdl": bool(o[24]),
-                "thread_rows": {"A": bool(o[25] & 1), "At": bool(o[25] & 2)}}
+                "thread_rows": {"A": bool(o[25] & 1), "At": bool(o[25] & 2)},
+                "segments": {"A": int(o[26] & 0xffff), "At": int(o[26] >> 16)}}
 
     def finish(self) -> SolutionReport:
         def fn(view, cc, rep, x, y, rc_, hist, cap):

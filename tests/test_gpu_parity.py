@@ -268,6 +268,44 @@ def test_spmv_engines_and_gather_policies(gpu, lp, monkeypatch):
         assert a.iterations == b.iterations and np.array_equal(a.x, b.x) and np.array_equal(a.y, b.y)
 
 
+SEG_LPS = [c1_small(m=300, n=500), c3_transport(S=40, T=70)]
+
+
+@pytest.mark.parametrize("lp", SEG_LPS, ids=[c.name for c in SEG_LPS])
+def test_column_segments_match_oracle(gpu, lp, monkeypatch):
+    """Column-segmented operators (built after scaling when the gathered
+    vector exceeds RHP_SEG_BYTES; forced here with a 1 KB segment): SpMV
+    within 1e-13 of the oracle, solves that match the reference (objective
+    1e-6, KKT at eps, first iterates 1e-10) and stay deterministic."""
+    monkeypatch.setenv("RHP_SEG_BYTES", "1024")
+    monkeypatch.setenv("RHP_SEG_FORCE", "1")
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, lp.num_vars)
+    y = rng.uniform(-1, 1, lp.num_cons)
+    O = support.oracle()
+    with DeviceContext(lp) as dev:
+        dev.scale(enabled=False)
+        lay = dev.layout()
+        ax, aty = dev.spmv(x), dev.spmv(y, True)
+    assert lay["segments"]["A"] == -(-lp.num_vars * 8 // 1024)
+    assert lay["segments"]["At"] == max(1, -(-lp.num_cons * 8 // 1024))
+    assert max_rel(ax, support.spmv_with(O, lp, x)) <= 1e-13
+    assert max_rel(aty, support.spmv_with(O, lp, y, True)) <= 1e-13
+    cfg = SolverConfig(epsilon=1e-8)
+    g = solve(lp, cfg)
+    o = support.solve_with(O, lp, cfg)
+    assert g.status == o.status == "optimal"
+    assert abs(g.objective - o.objective) <= 1e-6 * max(1.0, abs(o.objective))
+    k = support.kkt_with(O, lp, g.x, g.y)
+    assert k["gap_rel"] <= 1e-8 and k["primal_rel"] <= 1e-8
+    for it in (1, 10, 30):
+        cfg_it = SolverConfig(epsilon=1e-300, iteration_limit=it)
+        gi, oi = solve(lp, cfg_it), support.solve_with(O, lp, cfg_it)
+        assert max_rel(gi.x, oi.x) <= 1e-10 and max_rel(gi.y, oi.y) <= 1e-10
+    g2 = solve(lp, cfg)
+    assert g2.iterations == g.iterations and np.array_equal(g2.x, g.x)
+
+
 def test_operator_budget_and_counters(gpu):
     lp = support.lp_from_json(RANDOM[1]["lp"])
     r = solve(lp, SolverConfig(epsilon=1e-6))

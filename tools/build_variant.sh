@@ -11,7 +11,7 @@ mkdir -p $out
 PKG=paper_2507_14051_b200
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
   -Xcompiler -fPIC -Iinclude -Xptxas -v --expt-relaxed-constexpr -DRHP_WITH_NCCL "$@" \
-  -shared -o $out/librhp_cuda.so $PKG/csrc/rhp_cuda.cu $PKG/csrc/layout.cu $PKG/csrc/ingest.cu -ldl 2> $out/ptxas.log \
+  -shared -o $out/librhp_cuda.so $PKG/csrc/rhp_cuda.cu $PKG/csrc/layout.cu $PKG/csrc/ingest.cu $PKG/csrc/segments.cu -ldl 2> $out/ptxas.log \
   || (cat $out/ptxas.log; exit 1)
 g++ -std=c++20 -O2 -fPIC -Iinclude -I$PKG/host -shared -o $out/librhpdhg.so $PKG/host/*.cpp \
   -L$out -lrhp_cuda -lz -Wl,-rpath,'$ORIGIN'

@@ -125,7 +125,11 @@ def test_row_partition_exchange_matches_single_process_gloo():
                                        support.load_golden("random_feasible.json")
                                        ["instances"][-1]["lp"])],
                          ids=["c1_small", "ragged_long_rows", "rfl_5002"])
-def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker):
+@pytest.mark.parametrize("segments", [False, True], ids=["whole", "column_segments"])
+def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker, segments, monkeypatch):
+    if segments:  # both paths with forced 1 KB column segments
+        monkeypatch.setenv("RHP_SEG_BYTES", "1024")
+        monkeypatch.setenv("RHP_SEG_FORCE", "1")
     lp = maker()
     cfg = SolverConfig(epsilon=1e-7, record_residual_history=True)
     try:

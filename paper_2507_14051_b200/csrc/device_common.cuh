@@ -64,9 +64,8 @@ __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((
 
 // Gather of the SpMV input vector. Default: L1::no_allocate — a random
 // gather over a vector much larger than L1 almost never hits, and allocating
-// evicts useful lines. L1G (chosen per operator by timing both at setup,
-// rhp_cuda.cu tune_gathers): the read-only L1-allocating path, for vectors
-// that fit L1 (C3's A^T gathers a 16 KB y) or columns clustered within rows.
+// evicts useful lines. L1G (RHP_L1_GATHER=1, rhp_cuda.cu
+// choose_gather_policy): the read-only L1-allocating path.
 #ifndef RHP_GATHER_MODE
 #define RHP_GATHER_MODE 2
 #endif

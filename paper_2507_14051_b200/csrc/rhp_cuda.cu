@@ -117,7 +117,7 @@ struct DevOp : DeviceCsr {
   int32_t *head_slot = nullptr, *tail_slot = nullptr, *slot_first = nullptr, *slot_count = nullptr;
   double *slot_part = nullptr, *long_red = nullptr;
   unsigned int* slot_ticket = nullptr;
-  bool l1g = false;  // L1-allocating gathers (tune_gathers)
+  bool l1g = false;  // L1-allocating gathers (choose_gather_policy)
   // column segments (segments.cuh, build_segments): when non-empty the SpMV
   // walks segs[0..S-1] in order, the last one with the real epilogue, and
   // every schedule-dependent use goes through fin() (the last segment)
@@ -491,38 +491,15 @@ void build_segments(rhp_ctx& c, DevOp& d, const HostOperator& h, int64_t cols, i
   }
 }
 
-// Gather cache policy per operator (ld_gather): RHP_L1_GATHER=0/1 forces it;
-// otherwise both variants of the plain SpMV are timed once at setup (one
-// warm-up, then the best of `reps`) and the faster is kept. The policy only
-// changes which cache the gathered values pass through, never a result.
-// Measured: C2 keeps no_allocate on both operators (random columns over an
-// 8 MB / 4 MB vector); C3's A^T (16 KB y) and both C4 operators (columns
-// clustered per commodity / edge) take L1: C4 718 -> 844 iter/s.
-void tune_gathers(rhp_ctx& c) {
+// Gather cache policy (ld_gather): L1::no_allocate by default; RHP_L1_GATHER=1
+// selects the L1-allocating variant. A timing-based choice per operator was
+// used while the gathers had the default L2 policy (C4 gained 17 % from L1);
+// with evict_last gathers L1 no longer wins anywhere (C2 6958 vs 6620, C3
+// 22.9k both, C4 1102 vs 1076 iter/s), so the policy is fixed and
+// deterministic. The policy never changes a result.
+void choose_gather_policy(rhp_ctx& c) {
   const char* env = std::getenv("RHP_L1_GATHER");
-  if (env && (env[0] == '0' || env[0] == '1')) {
-    c.A.l1g = c.At.l1g = env[0] == '1';
-    return;
-  }
-  struct Case { DevOp* op; int grid; const double* in; double* out; };
-  const Case cases[2] = {{&c.A, c.grid_a, c.pv, c.pav}, {&c.At, c.grid_at, c.pav, c.pw}};
-  for (const Case& k : cases) {
-    if (k.op->nnz == 0) continue;
-    const int reps = k.op->nnz > (int64_t)100000000 ? 3 : 8;
-    float best[2] = {1e30f, 1e30f};
-    for (int r = -1; r < reps; ++r)  // variants alternate, so drift hits both; r = -1 warms up
-      for (int variant = 0; variant < 2; ++variant) {
-        k.op->l1g = variant == 1;
-        CK(cudaEventRecord(c.tev0, c.stream));
-        launch_spmv(c, *k.op, k.grid, k.in, store_into(k.out), nullptr, nullptr, c.stream);
-        CK(cudaEventRecord(c.tev1, c.stream));
-        CK(cudaEventSynchronize(c.tev1));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, c.tev0, c.tev1));
-        if (r >= 0) best[variant] = std::min(best[variant], ms);
-      }
-    k.op->l1g = best[1] < 0.97f * best[0];  // L1 only on a clear win
-  }
+  c.A.l1g = c.At.l1g = env && env[0] == '1';
 }
 
 EpiDual epi_dual(rhp_ctx& c, int token) {
@@ -985,7 +962,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     c->hist = dev_alloc<double>(static_cast<size_t>(opt.block_limit));
     if (const char* e = std::getenv("RHP_PDL")) c->pdl = e[0] == '1';
     choose_engines(*c);
-    tune_gathers(*c);
+    choose_gather_policy(*c);
     phase("engines+gather tuning");
     CK(cudaMalloc(&c->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&c->ctl_host, sizeof(Ctl)));

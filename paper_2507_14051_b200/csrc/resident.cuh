@@ -31,7 +31,10 @@
 
 namespace rhp {
 
-constexpr int kResThreads = 256;
+#ifndef RHP_RES_THREADS
+#define RHP_RES_THREADS 256
+#endif
+constexpr int kResThreads = RHP_RES_THREADS;
 constexpr int kResWarps = kResThreads / 32;
 constexpr int kResMaxCtas = 16;
 constexpr size_t kResSmemMax = 200 * 1024;  // per-CTA matrix slices must fit

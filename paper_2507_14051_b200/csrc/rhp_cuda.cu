@@ -620,7 +620,8 @@ bool setup_resident(rhp_ctx& c) {
   cfg.dynamicSmemBytes = kResSmemMax;
   int max_cluster = 1;
   CK(cudaOccupancyMaxPotentialClusterSize(&max_cluster, fn, &cfg));
-  const int ctas = std::max(1, std::min(kResMaxCtas, max_cluster));
+  int ctas = std::max(1, std::min(kResMaxCtas, max_cluster));
+  if (const char* e = std::getenv("RHP_RES_CTAS")) ctas = std::max(1, std::min(ctas, std::atoi(e)));
   const std::vector<int32_t> sa = split_rows(c.L.A.rp, ctas);
   const std::vector<int32_t> st = split_rows(c.L.At.rp, ctas);
   size_t need = 0;

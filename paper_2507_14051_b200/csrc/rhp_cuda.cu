@@ -620,17 +620,29 @@ bool setup_resident(rhp_ctx& c) {
   cfg.dynamicSmemBytes = kResSmemMax;
   int max_cluster = 1;
   CK(cudaOccupancyMaxPotentialClusterSize(&max_cluster, fn, &cfg));
-  int ctas = std::max(1, std::min(kResMaxCtas, max_cluster));
-  if (const char* e = std::getenv("RHP_RES_CTAS")) ctas = std::max(1, std::min(ctas, std::atoi(e)));
-  const std::vector<int32_t> sa = split_rows(c.L.A.rp, ctas);
-  const std::vector<int32_t> st = split_rows(c.L.At.rp, ctas);
+  // the smallest cluster of {8, 16} CTAs whose slices fit: fewer CTAs make
+  // the two cluster barriers and the DSMEM reductions cheaper (C1: 16 CTAs
+  // 112k, 8 CTAs 123k, 4 CTAs 90k iter/s); RHP_RES_CTAS caps the size
+  int cap = std::max(1, std::min(kResMaxCtas, max_cluster));
+  if (const char* e = std::getenv("RHP_RES_CTAS")) cap = std::max(1, std::min(cap, std::atoi(e)));
+  int ctas = 0;
+  std::vector<int32_t> sa, st;
   size_t need = 0;
-  for (int r = 0; r < ctas; ++r)  // matrix slices + the shared-memory iterate slices
-    need = std::max(need, slice_bytes(c.L.A.rp, sa[r], sa[r + 1]) +
-                              slice_bytes(c.L.At.rp, st[r], st[r + 1]) +
-                              8 * (6 * static_cast<size_t>(sa[r + 1] - sa[r]) +
-                                   7 * static_cast<size_t>(st[r + 1] - st[r])));
-  if (need > kResSmemMax) return false;
+  for (int cand : {std::min(8, cap), cap}) {
+    sa = split_rows(c.L.A.rp, cand);
+    st = split_rows(c.L.At.rp, cand);
+    need = 0;
+    for (int r = 0; r < cand; ++r)  // matrix slices + the shared-memory iterate slices
+      need = std::max(need, slice_bytes(c.L.A.rp, sa[r], sa[r + 1]) +
+                                slice_bytes(c.L.At.rp, st[r], st[r + 1]) +
+                                8 * (6 * static_cast<size_t>(sa[r + 1] - sa[r]) +
+                                     7 * static_cast<size_t>(st[r + 1] - st[r])));
+    if (need <= kResSmemMax) {
+      ctas = cand;
+      break;
+    }
+  }
+  if (ctas == 0) return false;
   c.res_ctas = ctas;
   c.res_smem = std::max<size_t>(need, 16);
   c.res_a_split = dev_alloc<int32_t>(sa.size());

@@ -26,7 +26,8 @@
 //        iteration (after a KKT check or restart changed aty, tau or the
 //        anchor), with K2's exact row->thread map so its partials are
 //        bit-identical to K2's.
-// Epilogue inputs arrive through the TMA-staged tile (spmv.cuh): input k of
+// The engines (spmv.cuh) call Epi::row(i, rowsum, e, stride, acc) once per
+// row with the row's epilogue inputs loaded by the finishing lane: input k of
 // row i is e[k*stride].
 #pragma once
 

@@ -302,7 +302,13 @@ def run_product(args):
     checks = b["kkt_checks"] - a["kkt_checks"]
     # per iteration: K1, K2 (+ control and K2c kernels on the partitioned path);
     # per block K3; per check 2 (partitioned: 4)
-    per_it, per_chk = (2, 2) if dist.world == 1 else (4, 4)
+    # (column-segmented operators: one launch per segment; cluster-resident
+    # small LPs: one launch per block)
+    seg = layout.get("segments", {"A": 1, "At": 1})
+    per_it, per_chk = ((seg["A"] + seg["At"], seg["A"] + seg["At"]) if dist.world == 1
+                       else (seg["A"] + seg["At"] + 2, seg["A"] + seg["At"] + 2))
+    if layout.get("resident"):
+        per_it = 0
     launches = per_it * iters + blocks + per_chk * checks
     t_max = dist.max(ms / 1e3)
     # one LP solved by all ranks together: the job's unit is a PDHG iteration

@@ -135,6 +135,8 @@ typedef struct rhp_layout_info {
   int32_t pdl;          /* SpMVs use programmatic dependent launch */
   int32_t thread_rows;  /* bit 0: A uses the thread-per-row engine, bit 1: A^T (last segment) */
   int32_t segments;     /* column segments: A's in bits 0-15, A^T's in bits 16-31 (1 = unsegmented) */
+  int32_t resident;     /* blocks run as one cluster-resident kernel (small LPs) */
+  int32_t pad_;
 } rhp_layout_info;
 
 const char* rhp_last_error(void);

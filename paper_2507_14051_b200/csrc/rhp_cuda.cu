@@ -1067,6 +1067,7 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->gather_l1 = (c->A.l1g ? 1 : 0) | (c->At.l1g ? 2 : 0);
     info->pdl = c->pdl ? 1 : 0;
     info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0);
+    info->resident = c->resident ? 1 : 0;
     info->segments = static_cast<int32_t>(std::max<size_t>(1, c->A.segs.size()) |
                                           (std::max<size_t>(1, c->At.segs.size()) << 16));
   });

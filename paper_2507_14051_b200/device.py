@@ -62,7 +62,8 @@ class DeviceContext:
                 "gather_l1": {"A": bool(info.gather_l1 & 1), "At": bool(info.gather_l1 & 2)},
                 "pdl": bool(info.pdl),
                 "thread_rows": {"A": bool(info.thread_rows & 1), "At": bool(info.thread_rows & 2)},
-                "segments": {"A": info.segments & 0xffff, "At": info.segments >> 16}}
+                "segments": {"A": info.segments & 0xffff, "At": info.segments >> 16},
+                "resident": bool(info.resident)}
 
     def scale(self, enabled=True, ruiz=10, pock_chambolle=True):
         self._ok(self.lib.rhp_scale(self.h, int(enabled), ruiz, int(pock_chambolle)))

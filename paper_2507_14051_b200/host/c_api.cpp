@@ -283,6 +283,7 @@ int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
     o[24] = li.pdl;
     o[25] = li.thread_rows;
     o[26] = li.segments;
+    o[27] = li.resident;
   });
 }
 

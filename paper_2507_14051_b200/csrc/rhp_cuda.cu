@@ -26,6 +26,7 @@
 #include "ingest.cuh"
 #include "layout.cuh"
 #include "pdhg_kernels.cuh"
+#include "peer.cuh"
 #include "resident.cuh"
 #include "scaling_kernels.cuh"
 #include "segments.cuh"
@@ -164,6 +165,12 @@ struct rhp_ctx {
   std::vector<int64_t> offsets;  // world+1 row offsets of the partition
   int64_t max_local = 0;         // largest local row count
   double* xchg = nullptr;        // [n + 16]: A_p^T partial | scalar sums (allreduced)
+  // peer-memory exchange (peer.cuh, RHP_PEER_EXCHANGE=1): xchg then lives in
+  // an IPC-shared region; peers' regions are opened at create
+  bool peer = false;
+  PeerView peerv{};
+  std::vector<void*> peer_opened;
+  unsigned int* peer_ticket = nullptr;
   double* ypad = nullptr;        // [max_local]
   double* ygather = nullptr;     // [world * max_local]
   int64_t* agree = nullptr;      // 1 int64 for host-decision agreement
@@ -502,6 +509,55 @@ void choose_gather_policy(rhp_ctx& c) {
   c.A.l1g = c.At.l1g = env && env[0] == '1';
 }
 
+// Peer-memory exchange (peer.cuh): one cudaMalloc'd region per rank, its
+// CUDA IPC handle all-gathered over the rank's NCCL communicator, the peers'
+// regions opened and mapped. The local xchg moves into the region.
+void setup_peers(rhp_ctx& c) {
+#ifdef RHP_WITH_NCCL
+  if (c.world > kMaxPeers) throw CudaError("peer exchange supports at most 16 ranks");
+  const size_t n = static_cast<size_t>(c.n);
+  const size_t doubles = (n + 16) + n + 8;
+  const size_t bytes = doubles * sizeof(double) + 2 * kMaxPeers * sizeof(unsigned long long);
+  void* region = nullptr;
+  CK(cudaMalloc(&region, bytes));
+  CK(cudaMemset(region, 0, bytes));
+  cudaIpcMemHandle_t mine;
+  CK(cudaIpcGetMemHandle(&mine, region));
+  char* d_h = nullptr;
+  CK(cudaMalloc(&d_h, sizeof(mine) * (c.world + 1)));
+  CK(cudaMemcpy(d_h, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  if (nccl().AllGather(d_h, d_h + sizeof(mine), sizeof(mine), ncclChar, c.comm, c.stream) != ncclSuccess)
+    throw CudaError("ncclAllGather of the IPC handles failed");
+  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(c.world));
+  CK(cudaMemcpyAsync(all.data(), d_h + sizeof(mine), sizeof(mine) * c.world, cudaMemcpyDeviceToHost,
+                     c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaFree(d_h));
+  for (int q = 0; q < c.world; ++q) {
+    void* ptr = region;
+    if (q != c.rank) {
+      CK(cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess));
+      c.peer_opened.push_back(ptr);
+    }
+    double* base = static_cast<double*>(ptr);
+    c.peerv.xchg[q] = base;
+    c.peerv.rbuf[q] = base + n + 16;
+    c.peerv.flags[q] = reinterpret_cast<unsigned long long*>(base + doubles);
+  }
+  c.peerv.ysum = static_cast<double*>(region) + 2 * n + 16;
+  c.peerv.rank = c.rank;
+  c.peerv.world = c.world;
+  c.peerv.n = c.n;
+  if (c.xchg) CK(cudaFree(c.xchg));
+  c.xchg = static_cast<double*>(region);
+  c.peer_ticket = dev_alloc<unsigned int>(1);
+  c.peer = true;
+#else
+  (void)c;
+  throw CudaError("built without NCCL");
+#endif
+}
+
 EpiDual epi_dual(rhp_ctx& c, int token) {
   EpiDual e{};
   e.ctl = c.ctl;
@@ -567,7 +623,14 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   st.ctl = c.ctl;
   st.token = token;
   launch_spmv(c, c.At, c.grid_at, c.yp, st, nullptr, nullptr, s);
-  allreduce(c, c.xchg, static_cast<size_t>(c.n) + 5, s);
+  if (c.peer) {  // A^T y exchange over NVLink peer memory (peer.cuh)
+    k_peer_signal<<<1, 32, 0, s>>>(c.ctl, token, c.peerv);
+    k_peer_reduce<<<c.grid_vec, kBlock, 0, s>>>(c.ctl, token, c.peerv, c.peer_ticket);
+    k_peer_gather<<<c.grid_vec, kBlock, 0, s>>>(c.ctl, token, c.peerv);
+    CK(cudaGetLastError());
+  } else {
+    allreduce(c, c.xchg, static_cast<size_t>(c.n) + 5, s);
+  }
   k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, c.grid_at, fin(c.At).sched.n_multi,
                                       fin(c.At).long_red, c.xchg + c.n, token);
   CK(cudaGetLastError());
@@ -1008,6 +1071,7 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       std::memcpy(&id, opt.nccl_id, sizeof(id));
       if (nccl().CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess)
         throw CudaError("ncclCommInitRank failed");
+      if (const char* e = std::getenv("RHP_PEER_EXCHANGE"); e && e[0] == '1') setup_peers(*c);
 #else
       throw CudaError("built without NCCL");
 #endif
@@ -1026,6 +1090,8 @@ int rhp_destroy(rhp_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
+  for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
+  if (c->peer_ticket) cudaFree(c->peer_ticket);
   free_op(c->A);
   free_op(c->At);
   for (double* p : {c->c, c->vl, c->vu, c->cl, c->cu, c->co, c->vlo, c->vuo, c->clo, c->cuo,

@@ -126,10 +126,17 @@ def test_row_partition_exchange_matches_single_process_gloo():
                                        ["instances"][-1]["lp"])],
                          ids=["c1_small", "ragged_long_rows", "rfl_5002"])
 @pytest.mark.parametrize("segments", [False, True], ids=["whole", "column_segments"])
-def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker, segments, monkeypatch):
+@pytest.mark.parametrize("exchange", ["nccl", "peer"])
+def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker, segments, exchange,
+                                                         monkeypatch):
+    """One rank of the row-partitioned engine (NCCL allreduce, or the
+    NVLink peer-memory exchange of peer.cuh with the rank as its own peer)
+    reproduces the single-GPU solve bit for bit."""
     if segments:  # both paths with forced 1 KB column segments (DESIGN.md §4)
         monkeypatch.setenv("RHP_SEG_BYTES", "1024")
         monkeypatch.setenv("RHP_SEG_FORCE", "1")
+    if exchange == "peer":
+        monkeypatch.setenv("RHP_PEER_EXCHANGE", "1")
     lp = maker()
     cfg = SolverConfig(epsilon=1e-7, record_residual_history=True)
     try:
@@ -146,3 +153,69 @@ def test_partitioned_path_one_rank_is_bitwise_single_gpu(gpu, maker, segments, m
     assert np.array_equal(part.x, single.x) and np.array_equal(part.y, single.y)
     assert np.array_equal(part.fixed_point_residual_history, single.fixed_point_residual_history)
     assert part.matrix_norm_estimate == single.matrix_norm_estimate
+
+
+def _peer_worker(rank, world, port, q):
+    """The peer-memory exchange of peer.cuh restated over gloo: every rank
+    publishes its partial, reduces the columns it owns (slice n*r/P ..
+    n*(r+1)/P, the formula of owned_slice) over all partials in rank order,
+    and gathers every owner's slice."""
+    import torch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        O = support.oracle()
+        lp = ragged()
+        off = partition_rows(lp, world)
+        loc = block(lp, int(off[rank]), int(off[rank + 1]))
+        y = np.random.default_rng(1).uniform(-1, 1, lp.num_cons)
+        y_loc = y[off[rank]:off[rank + 1]]
+        n = lp.num_vars
+        part = torch.from_numpy(np.concatenate([support.spmv_with(O, loc, y_loc, True),
+                                                [float(np.dot(y_loc, y_loc))]]))
+        # phase 1: every rank can read every partial (peer loads)
+        parts = [torch.zeros_like(part) for _ in range(world)]
+        dist.all_gather(parts, part)
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        own = parts[0][lo:hi].clone()
+        for p in parts[1:]:
+            own += p[lo:hi]  # rank order
+        ysum = parts[0][n:].clone()
+        for p in parts[1:]:
+            ysum += p[n:]
+        # phase 2: gather the owners' slices (variable sizes: pad to the largest)
+        width = -(-n // world) + 1
+        padded = torch.zeros(width, dtype=torch.float64)
+        padded[:hi - lo] = own
+        slices = [torch.zeros_like(padded) for _ in range(world)]
+        dist.all_gather(slices, padded)
+        full = torch.cat([slices[r][:n * (r + 1) // world - n * r // world] for r in range(world)])
+        ref = part.clone()
+        dist.all_reduce(ref)
+        q.put((rank, torch.cat([full, ysum]).numpy(), ref.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_protocol_gloo():
+    """Every rank ends with the same reduced vector (bitwise), equal to the
+    allreduce up to summation order and to the single-process A^T y."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, full, ref in res:
+        assert np.array_equal(full, res[0][1])  # identical on every rank
+        assert np.allclose(full, ref, rtol=1e-13, atol=1e-13)
+    lp = ragged()
+    y = np.random.default_rng(1).uniform(-1, 1, lp.num_cons)
+    aty = support.spmv_with(support.oracle(), lp, y, True)
+    assert np.allclose(res[0][1][:-1], aty, rtol=1e-12, atol=1e-12)

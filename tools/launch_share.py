@@ -40,9 +40,15 @@ def main():
     out = [f"# Launch list share{(' — ' + args.title) if args.title else ''}", "",
            f"Source: `{args.csv}` (ncu gpu__time_duration.sum, --clock-control none; cold-cache, serialised "
            "launches, so only the shares are comparable with live timings).", "",
-           "| kernel | launches | mean us | max us | share of device time |", "|---|---|---|---|---|"]
+           "Profiled with plain launches (`--no-graph`): a block enqueues its iterations up to the next "
+           "scheduled check, and launches past an earlier stop (a restart verdict) exit at entry — the "
+           "short launches; 'working' = launches taking at least half of the kernel's maximum.", "",
+           "| kernel | launches | working | mean us (working) | max us | share of device time |",
+           "|---|---|---|---|---|---|"]
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-        out.append(f"| {k} | {len(v)} | {sum(v) / len(v):.1f} | {max(v):.1f} | {sum(v) / tot:.3f} |")
+        w = [t for t in v if t >= 0.5 * max(v)]
+        out.append(f"| {k} | {len(v)} | {len(w)} | {sum(w) / len(w):.1f} | {max(v):.1f} | "
+                   f"{sum(v) / tot:.3f} |")
     text = "\n".join(out) + "\n"
     if args.out:
         open(args.out, "w").write(text)

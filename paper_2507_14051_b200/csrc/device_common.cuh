@@ -132,6 +132,9 @@ constexpr double kGatherL2Bytes = 32.0 * 1024 * 1024;
 // Operators whose longest row has at most kThreadRowMax nonzeros use the
 // thread-per-row engine (spmv.cuh thread_rows; rhp_cuda.cu choose_engines).
 constexpr int64_t kThreadRowMax = 8;
+#ifndef RHP_ROWS_IN_FLIGHT
+#define RHP_ROWS_IN_FLIGHT 2
+#endif
 
 // K1/K2 pairs per body of the block graph's WHILE node (one conditional
 // evaluation per body; copies after a stop exit at entry). C2: 2 -> 6893,

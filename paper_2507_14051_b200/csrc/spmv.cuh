@@ -283,7 +283,7 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
 // Thread-per-row engine, for operators whose rows are all short
 // (Sched::thread_rows: max row length <= kThreadRowMax, chosen at setup —
 // C3's A^T rows have 2 nonzeros, C4's 3). Thread g of the grid owns rows g,
-// g + G, g + 2G, ... (G = threads of the grid), two rows in flight per
+// g + G, g + 2G, ... (G = threads of the grid), RHP_ROWS_IN_FLIGHT (2) rows in flight per
 // thread. No scan, no shared memory and no split rows: a row's products are
 // summed sequentially in element order — the reference's own order
 // (sparse_matrix.cpp:67-87), so these row sums are bit-identical to its — and
@@ -295,50 +295,61 @@ __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* val
                                             const double* __restrict__ xg, const Sched& s,
                                             Epi& epi, double (&acc)[Epi::NRED]) {
   constexpr int NI = Epi::NIN > 0 ? Epi::NIN : 1;
+  constexpr int RF = RHP_ROWS_IN_FLIGHT;  // rows in flight per thread
+  constexpr int EC = RF >= 4 ? 2 : 4;     // elements per row per step
   const int64_t G = static_cast<int64_t>(gridDim.x) * kBlock;
   const int64_t R = s.rows;
-  for (int64_t i1 = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x; i1 < R; i1 += 2 * G) {
-    const int64_t i2 = i1 + G;
-    const bool two = i2 < R;
-    double e1[NI], e2[NI];
-    load_inputs(epi, i1, e1);
-    if (two) load_inputs(epi, i2, e2);
-    double s1 = 0.0, s2 = 0.0;
-    if constexpr (!WALK) {
-      const int64_t lo1 = s.rp[i1], hi1 = s.rp[i1 + 1];
-      const int64_t lo2 = two ? s.rp[i2] : 0, hi2 = two ? s.rp[i2 + 1] : 0;
-      const int64_t len = max(hi1 - lo1, hi2 - lo2);
-      for (int64_t t = 0; t < len; t += 4) {
-        int c1[4], c2[4];
-        double v1[4], v2[4], g1[4], g2[4];
+  // thread g owns rows g, g + G, g + 2G, ... and finishes them in that order
+  // whatever RF is, so the reductions do not depend on RF
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x; i0 < R; i0 += RF * G) {
+    double e[RF][NI], sm[RF];
+    int64_t lo[RF], hi[RF];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool ok1 = lo1 + t + u < hi1, ok2 = lo2 + t + u < hi2;
-          c1[u] = ok1 ? __ldcs(ci + lo1 + t + u) : 0;
-          v1[u] = ok1 ? __ldcs(vals + lo1 + t + u) : 0.0;
-          c2[u] = ok2 ? __ldcs(ci + lo2 + t + u) : 0;
-          v2[u] = ok2 ? __ldcs(vals + lo2 + t + u) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          g1[u] = lo1 + t + u < hi1 ? ld_gather<L1G>(xg + c1[u]) : 0.0;
-          g2[u] = lo2 + t + u < hi2 ? ld_gather<L1G>(xg + c2[u]) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (lo1 + t + u < hi1) s1 = add(s1, mul(v1[u], g1[u]));
-          if (lo2 + t + u < hi2) s2 = add(s2, mul(v2[u], g2[u]));
-        }
-      }
+    for (int f = 0; f < RF; ++f) {
+      const int64_t i = i0 + f * G;
+      if (i < R) load_inputs(epi, i, e[f]);
+      sm[f] = 0.0;
     }
     if constexpr (!WALK) {
+      int64_t len = 0;
+#pragma unroll
+      for (int f = 0; f < RF; ++f) {
+        const int64_t i = i0 + f * G;
+        lo[f] = i < R ? s.rp[i] : 0;
+        hi[f] = i < R ? s.rp[i + 1] : 0;
+        len = max(len, hi[f] - lo[f]);
+      }
+      for (int64_t t = 0; t < len; t += EC) {
+        int c[RF][EC];
+        double v[RF][EC], g[RF][EC];
+#pragma unroll
+        for (int f = 0; f < RF; ++f)
+#pragma unroll
+          for (int u = 0; u < EC; ++u) {
+            const bool ok = lo[f] + t + u < hi[f];
+            c[f][u] = ok ? __ldcs(ci + lo[f] + t + u) : 0;
+            v[f][u] = ok ? __ldcs(vals + lo[f] + t + u) : 0.0;
+          }
+#pragma unroll
+        for (int f = 0; f < RF; ++f)
+#pragma unroll
+          for (int u = 0; u < EC; ++u)
+            g[f][u] = lo[f] + t + u < hi[f] ? ld_gather<L1G>(xg + c[f][u]) : 0.0;
+#pragma unroll
+        for (int f = 0; f < RF; ++f)
+#pragma unroll
+          for (int u = 0; u < EC; ++u)
+            if (lo[f] + t + u < hi[f]) sm[f] = add(sm[f], mul(v[f][u], g[f][u]));
+      }
       if (s.seg_in) {
-        s1 = add(__ldcg(s.seg_in + i1), s1);
-        if (two) s2 = add(__ldcg(s.seg_in + i2), s2);
+#pragma unroll
+        for (int f = 0; f < RF; ++f)
+          if (i0 + f * G < R) sm[f] = add(__ldcg(s.seg_in + i0 + f * G), sm[f]);
       }
     }
-    epi.row(i1, s1, e1, 1, acc);
-    if (two) epi.row(i2, s2, e2, 1, acc);
+#pragma unroll
+    for (int f = 0; f < RF; ++f)
+      if (i0 + f * G < R) epi.row(i0 + f * G, sm[f], e[f], 1, acc);
   }
 }
 

@@ -10,7 +10,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas 
             --expt-relaxed-constexpr -DRHP_WITH_NCCL
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/host
 
-CU_SRCS  := $(PKG)/csrc/rhp_cuda.cu $(PKG)/csrc/layout.cu $(PKG)/csrc/ingest.cu $(PKG)/csrc/segments.cu
+CU_SRCS  := $(PKG)/csrc/rhp_cuda.cu $(PKG)/csrc/layout.cu $(PKG)/csrc/ingest.cu $(PKG)/csrc/segments.cu $(PKG)/csrc/ops.cu
 CU_HDRS  := $(wildcard $(PKG)/csrc/*.cuh) include/rhpdhg_cuda.h include/rhpdhg_c.h
 HOST_SRCS:= $(wildcard $(PKG)/host/*.cpp)
 HOST_HDRS:= $(wildcard $(PKG)/host/*.hpp) $(wildcard include/rhpdhg/*.hpp) include/rhpdhg_c.h include/rhpdhg_cuda.h

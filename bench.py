@@ -176,7 +176,8 @@ WORKLOADS = {
     "c1": "C1 synthetic feasible bounded LP (m=1k, n=2k, ~10k nnz)",
     "c2": "C2 synthetic MIPLIB-relaxation-like LP (m=500k, n=1M, ~10M nnz, power-law rows)",
     "c3": "C3 synthetic transportation LP (1k x 1k, n=1M, 2M nnz)",
-    "c4": "C4 synthetic multicommodity-flow LP (K=20, E=1M, n=20M, 60M nnz)",
+    "c4": "C4 synthetic multicommodity-flow LP (K=25 commodities x 40 terminal pairs, V=200k, "
+          "E=1M, n=25M, m=6.2M, 100M nnz; binding arc capacities + node capacities)",
     "c5": "C5 synthetic row-partitionable LP (m=50M, n=20M, ~1B nnz, power-law rows)",
 }
 # C5's CPU sample: the reference on the same generator at 1/50 scale (20M
@@ -383,6 +384,7 @@ def run_product(args):
                "time_to_tol_s": t_e2e, "tol": args.e2e_eps,
                "time_to_1e-4_s": t_1e4, "iterations_to_1e-4": it_1e4 if t_1e4 else None,
                "setup_s": t_setup, "power_iterations": rep.power_iterations,
+               "final_primal_weight": rep.final_primal_weight,
                "objective": rep.objective,
                "residuals": vars(rep.residuals)}
 

@@ -22,6 +22,9 @@
  *   rhp_kkt             kkt_check + kkt_residuals sums   src/solver.cpp:32-49, src/termination.cpp:58-118
  *   rhp_restart         do_restart (anchor, k, residuals) src/restart.cpp:71-83
  *   rhp_spmv            SparseMatrix::multiply{,_transpose} src/sparse_matrix.cpp:67-87
+ *   rhp_op_pdhg         pdhg_step, halpern_reflected_step src/pdhg.cpp:34-65, src/restart.cpp:35-52
+ *   rhp_op_sums         quadratic_form / distance2 / norm2 sums src/pdhg.cpp:68-75, src/restart.cpp:8-21
+ *   rhp_op_mul          unscale_iterate                   src/scaling.cpp:83-94
  * The PID weight update (src/restart.cpp:85-120), the termination test
  * (src/termination.cpp:120-124) and all exception mapping stay on the host.
  *
@@ -215,6 +218,55 @@ int rhp_gather_ceiling(rhp_ctx* ctx, int reps, double* ms_a, double* ms_at);
 int rhp_profiler_range(int start);
 /* Synchronize the ctx stream. */
 int rhp_synchronize(rhp_ctx* ctx);
+
+
+/* ---- per-operation API -------------------------------------------------
+ * The reference's per-op functions (pdhg.hpp:44-58 pdhg_step / p_norm /
+ * fixed_point_residual, restart.hpp:47-70 halpern_reflected_step /
+ * pid_update, scaling.hpp:30-32 unscale_iterate) as device round trips of
+ * host vectors in original order. A ctx passed here is a product context of
+ * one matrix (never rhp_scale'd); the host library caches one per
+ * SparseMatrix. Elementwise formulas are bit-identical to the reference's;
+ * products and sums use the device engines (reduction-order drift only). */
+typedef struct rhp_op_lp {
+  const double *objective, *var_lb, *var_ub; /* [n] */
+  const double *con_lb, *con_ub;             /* [m] */
+} rhp_op_lp;
+typedef struct rhp_op_iter {
+  const double *x, *y, *ax, *aty; /* x, aty: [n]; y, ax: [m] */
+} rhp_op_iter;
+typedef struct rhp_op_out {
+  double *x, *y, *ax, *aty;
+} rhp_op_out;
+/* tau = eta/omega, sigma = eta*omega, sigma_inv = 1/sigma (pdhg.cpp:35-50);
+ * a = (k+1)/(k+2), b = 1/(k+2), gamma (restart.cpp:38-40). */
+typedef struct rhp_op_params {
+  double tau, sigma, sigma_inv, gamma, a, b;
+} rhp_op_params;
+
+/* pdhg_step (pdhg.cpp:34-65) of z: inner = (x+, y+, A x+, A^T y+),
+ * dx = x - x+, dy = y - y+ (dx/dy may be NULL). With anchor != NULL it is
+ * halpern_reflected_step (restart.cpp:35-52): znew = a((1+g) inner - g z)
+ * + b anchor for x, y, ax and aty. */
+int rhp_op_pdhg(rhp_ctx* ctx, const rhp_op_params* p, const rhp_op_lp* lp, const rhp_op_iter* z,
+                const rhp_op_iter* anchor, const rhp_op_out* inner, double* dx, double* dy,
+                const rhp_op_out* znew);
+/* CSC-order values of the matrix (the reference's csc_values(), which for a
+ * matrix produced by a scaling differ from the CSR values in the last ulp):
+ * scale_source 0 — A^T products of this (unscaled) ctx use them;
+ * scale_source 1 — rhp_scale applies its A^T scales to them (scaling.cpp:17
+ * matrix.scaled() scales each layout from its own values). */
+int rhp_set_csc_values(rhp_ctx* ctx, const double* csc_values, int scale_source);
+/* Replaces the objective and bounds of an unscaled ctx (kkt_residuals of a
+ * problem whose matrix has a cached product context). */
+int rhp_set_vectors(rhp_ctx* ctx, const rhp_op_lp* lp);
+/* Sums on the device (fixed order, run-to-run identical):
+ * out[0] = sum (p - pm)^2 (pm NULL: sum p^2), out[1] = sum q^2,
+ * out[2] = sum q (r - rs) (r NULL: 0, rs NULL: sum q r), out[3] = sum p^2. */
+int rhp_op_sums(int device, int64_t n, const double* p, const double* pm, int64_t m,
+                const double* q, const double* r, const double* rs, double* out4);
+/* out = s * v elementwise (unscale_iterate, scaling.cpp:83-94). */
+int rhp_op_mul(int device, int64_t n, const double* s, const double* v, double* out);
 
 #ifdef __cplusplus
 }

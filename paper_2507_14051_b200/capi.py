@@ -193,6 +193,7 @@ CUDA_SYMBOLS = [
     "rhp_partition_rows",
     "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_time_spmv", "rhp_gather_ceiling", "rhp_profiler_range",
     "rhp_synchronize",
+    "rhp_op_pdhg", "rhp_set_vectors", "rhp_set_csc_values", "rhp_op_sums", "rhp_op_mul",
 ]
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",

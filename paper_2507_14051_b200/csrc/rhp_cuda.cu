@@ -25,6 +25,7 @@
 
 #include "ingest.cuh"
 #include "layout.cuh"
+#include "op_kernels.cuh"
 #include "pdhg_kernels.cuh"
 #include "peer.cuh"
 #include "resident.cuh"
@@ -180,6 +181,14 @@ struct rhp_ctx {
   size_t res_smem = 0;
   int32_t *res_a_split = nullptr, *res_at_split = nullptr;
   bool pdl = false;  // programmatic dependent launch of the SpMVs (launch_spmv, RHP_PDL=1)
+  bool scaled = false;  // rhp_scale ran (it consumes the original values: once per ctx)
+  // per-operation API scratch (rhp_op_pdhg), allocated on first use:
+  // 12 n-vectors then 11 m-vectors
+  double* opbuf = nullptr;
+  // rhp_set_csc_values(.., 1): the input's own CSC values as the source of
+  // the A^T apply in rhp_scale (a matrix whose CSC values were produced by an
+  // earlier scaling differs from its CSR values in the last ulp)
+  double* csc_src = nullptr;
 #ifdef RHP_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -886,6 +895,12 @@ void exact_caches(rhp_ctx& c) {
 extern "C" {
 
 const char* rhp_last_error(void) { return g_err.c_str(); }
+}  // extern "C"
+
+// ops.cu reports its failures through the same thread-local message
+void rhp_internal_set_error(const std::string& msg) { g_err = msg; }
+
+extern "C" {
 
 int rhp_device_count(int* count) {
   return guarded([&] {
@@ -1100,6 +1115,8 @@ int rhp_destroy(rhp_ctx* c) {
                     c->part3, c->partA, c->partAt, c->hist, c->xchg, c->ypad, c->ygather})
     if (p) cudaFree(p);
   if (c->agree) cudaFree(c->agree);
+  if (c->opbuf) cudaFree(c->opbuf);
+  if (c->csc_src) cudaFree(c->csc_src);
   if (c->res_a_split) cudaFree(c->res_a_split);
   if (c->res_at_split) cudaFree(c->res_at_split);
 #ifdef RHP_WITH_NCCL
@@ -1142,6 +1159,10 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
 // ruiz_equilibrate + pock_chambolle_scale (scaling.cpp:46-81) on the device.
 int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) {
   return guarded([&] {
+    // the original values are consumed (freed below) and rs/cs accumulate:
+    // scaling twice would compound the scales from already-scaled values
+    if (c->scaled) throw std::invalid_argument("rhp_scale: the context is already scaled");
+    c->scaled = true;
     cudaStream_t s = c->stream;
     const int64_t m = c->m, n = c->n;
     const int gr = vec_grid(*c, std::max<int64_t>(m, n));
@@ -1168,7 +1189,8 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
       }
       // apply_scales(original, rs, cs): values and vectors from the originals
       k_scale_values<<<gr, kBlock, 0, s>>>(c->A.rp, c->A.ci, c->A.v_orig, c->A.v, m, c->rs, c->cs);
-      k_scale_values<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci, c->At.v_orig, c->At.v, n, c->cs,
+      k_scale_values<<<gr, kBlock, 0, s>>>(c->At.rp, c->At.ci,
+                                           c->csc_src ? c->csc_src : c->At.v_orig, c->At.v, n, c->cs,
                                            c->rs);
       k_apply_col_scales<<<gr, kBlock, 0, s>>>(c->c, c->vl, c->vu, c->cs, n);
       k_apply_row_scales<<<gr, kBlock, 0, s>>>(c->cl, c->cu, c->rs, m);
@@ -1199,6 +1221,8 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
     if (c->A.v_orig) CK(cudaFree(c->A.v_orig));
     if (c->At.v_orig) CK(cudaFree(c->At.v_orig));
     c->A.v_orig = c->At.v_orig = nullptr;
+    if (c->csc_src) CK(cudaFree(c->csc_src));
+    c->csc_src = nullptr;
     // column segments of the scaled operators (gathered vectors larger than L2)
     build_segments(*c, c->A, c->L.A, c->n, c->grid_a);
     build_segments(*c, c->At, c->L.At, c->m, c->grid_at);
@@ -1626,6 +1650,106 @@ int rhp_profiler_range(int start) {
 
 int rhp_synchronize(rhp_ctx* c) {
   return guarded([&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+// ---------------------------------------------------------------- per-op --
+// The reference's per-operation API as device round trips (rhpdhg_cuda.h).
+
+int rhp_set_vectors(rhp_ctx* c, const rhp_op_lp* lp) {
+  return guarded([&] {
+    if (c->scaled || c->dist)
+      throw std::invalid_argument("rhp_set_vectors: needs an unscaled single-GPU context");
+    cudaStream_t s = c->stream;
+    const std::vector<int32_t> lrows = local_rows(*c);
+    upload_perm(c->co, lp->objective, c->L.pcol, c->hbuf, s);
+    upload_perm(c->vlo, lp->var_lb, c->L.pcol, c->hbuf, s);
+    upload_perm(c->vuo, lp->var_ub, c->L.pcol, c->hbuf, s);
+    upload_perm(c->clo, lp->con_lb, lrows, c->hbuf, s);
+    upload_perm(c->cuo, lp->con_ub, lrows, c->hbuf, s);
+  });
+}
+
+int rhp_set_csc_values(rhp_ctx* c, const double* csc_values, int scale_source) {
+  return guarded([&] {
+    if (c->scaled || c->dist)
+      throw std::invalid_argument("rhp_set_csc_values: needs an unscaled single-GPU context");
+    const size_t nz = static_cast<size_t>(c->L.nnz);
+    if (!nz) return;
+    if (scale_source) {
+      if (!c->csc_src) c->csc_src = dev_alloc<double>(nz);
+      upload(c->csc_src, csc_values, nz, c->stream);
+    } else {
+      upload(c->At.v, csc_values, nz, c->stream);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rhp_op_pdhg(rhp_ctx* c, const rhp_op_params* p, const rhp_op_lp* lp, const rhp_op_iter* z,
+                const rhp_op_iter* anchor, const rhp_op_out* inner, double* dx, double* dy,
+                const rhp_op_out* znew) {
+  return guarded([&] {
+    if (c->scaled || c->dist)
+      throw std::invalid_argument("rhp_op_pdhg: needs an unscaled single-GPU context");
+    cudaStream_t s = c->stream;
+    const int64_t m = c->m, n = c->n;
+    const size_t mp = static_cast<size_t>(std::max<int64_t>(m, 1)) + 8;
+    const size_t np = static_cast<size_t>(std::max<int64_t>(n, 1)) + 8;
+    if (!c->opbuf) c->opbuf = dev_alloc<double>(12 * np + 11 * mp);
+    double* b = c->opbuf;
+    double *x = b, *aty = b + np, *cc = b + 2 * np, *lb = b + 3 * np, *ub = b + 4 * np,
+           *xp = b + 5 * np, *atyp = b + 6 * np, *ddx = b + 7 * np, *x0 = b + 8 * np,
+           *aty0 = b + 9 * np, *xn = b + 10 * np, *atyn = b + 11 * np;
+    double* bm = b + 12 * np;
+    double *y = bm, *ax = bm + mp, *cl = bm + 2 * mp, *cu = bm + 3 * mp, *yp = bm + 4 * mp,
+           *axp = bm + 5 * mp, *ddy = bm + 6 * mp, *y0 = bm + 7 * mp, *ax0 = bm + 8 * mp,
+           *yn = bm + 9 * mp, *axn = bm + 10 * mp;
+    const std::vector<int32_t> lrows = local_rows(*c);
+    upload_perm(x, z->x, c->L.pcol, c->hbuf, s);
+    upload_perm(aty, z->aty, c->L.pcol, c->hbuf, s);
+    upload_perm(y, z->y, lrows, c->hbuf, s);
+    upload_perm(ax, z->ax, lrows, c->hbuf, s);
+    upload_perm(cc, lp->objective, c->L.pcol, c->hbuf, s);
+    upload_perm(lb, lp->var_lb, c->L.pcol, c->hbuf, s);
+    upload_perm(ub, lp->var_ub, c->L.pcol, c->hbuf, s);
+    upload_perm(cl, lp->con_lb, lrows, c->hbuf, s);
+    upload_perm(cu, lp->con_ub, lrows, c->hbuf, s);
+    const int gn = vec_grid(*c, n), gm = vec_grid(*c, m);
+    // x+ = proj(x - tau(c - aty)); ax+ = A x+
+    k_op_primal<<<gn, kBlock, 0, s>>>(n, p->tau, x, aty, cc, lb, ub, xp);
+    CK(cudaGetLastError());
+    if (c->L.nnz > 0 && m > 0) launch_spmv(*c, c->A, c->grid_a, xp, store_into(axp), nullptr, nullptr, s);
+    else if (m > 0) CK(cudaMemsetAsync(axp, 0, static_cast<size_t>(m) * sizeof(double), s));
+    // y+ from the caches (2 ax+ - ax); aty+ = A^T y+
+    k_op_dual<<<gm, kBlock, 0, s>>>(m, p->sigma, p->sigma_inv, y, ax, axp, cl, cu, yp);
+    CK(cudaGetLastError());
+    if (c->L.nnz > 0 && n > 0) launch_spmv(*c, c->At, c->grid_at, yp, store_into(atyp), nullptr, nullptr, s);
+    else if (n > 0) CK(cudaMemsetAsync(atyp, 0, static_cast<size_t>(n) * sizeof(double), s));
+    k_op_sub<<<gn, kBlock, 0, s>>>(n, x, xp, ddx);
+    k_op_sub<<<gm, kBlock, 0, s>>>(m, y, yp, ddy);
+    CK(cudaGetLastError());
+    if (anchor && znew) {
+      upload_perm(x0, anchor->x, c->L.pcol, c->hbuf, s);
+      upload_perm(aty0, anchor->aty, c->L.pcol, c->hbuf, s);
+      upload_perm(y0, anchor->y, lrows, c->hbuf, s);
+      upload_perm(ax0, anchor->ax, lrows, c->hbuf, s);
+      k_op_affine<<<gn, kBlock, 0, s>>>(n, p->a, p->gamma, p->b, xp, x, x0, xn);
+      k_op_affine<<<gm, kBlock, 0, s>>>(m, p->a, p->gamma, p->b, yp, y, y0, yn);
+      k_op_affine<<<gm, kBlock, 0, s>>>(m, p->a, p->gamma, p->b, axp, ax, ax0, axn);
+      k_op_affine<<<gn, kBlock, 0, s>>>(n, p->a, p->gamma, p->b, atyp, aty, aty0, atyn);
+      CK(cudaGetLastError());
+      download_perm(znew->x, xn, c->L.pcol, c->hbuf, s);
+      download_perm(znew->y, yn, lrows, c->hbuf, s);
+      download_perm(znew->ax, axn, lrows, c->hbuf, s);
+      download_perm(znew->aty, atyn, c->L.pcol, c->hbuf, s);
+    }
+    download_perm(inner->x, xp, c->L.pcol, c->hbuf, s);
+    download_perm(inner->y, yp, lrows, c->hbuf, s);
+    download_perm(inner->ax, axp, lrows, c->hbuf, s);
+    download_perm(inner->aty, atyp, c->L.pcol, c->hbuf, s);
+    if (dx) download_perm(dx, ddx, c->L.pcol, c->hbuf, s);
+    if (dy) download_perm(dy, ddy, lrows, c->hbuf, s);
+  });
 }
 
 }  // extern "C"

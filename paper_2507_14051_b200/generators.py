@@ -125,38 +125,90 @@ def c3_transport(seed: int = 20240820, S: int = 1000, T: int = 1000) -> LpProble
 
 
 def c4_multicommodity(seed: int = 20240821, V: int = 200_000, E: int = 1_000_000,
-                      K: int = 20) -> LpProblem:
-    """C4: K-commodity min-cost flow on a random directed graph (V nodes, E
-    arcs incl. a Hamiltonian cycle for connectivity). Variables x_ke >= 0
-    (n = K*E); rows: conservation per (k, v) (equality, m1 = K*V) and shared
-    capacity per arc as [0, cap_e] (m2 = E). nnz = 3*K*E."""
+                      K: int = 25, terminals: int = 40) -> LpProblem:
+    """C4: K-commodity min-cost flow with shared arc and node capacities.
+
+    Random directed graph: V nodes, E arcs (a Hamiltonian cycle + E-V random
+    arcs). Variables x_ke >= 0, n = K*E, commodity-major (column k*E + e).
+    Rows (m = K*V + E + V, nnz = 4*K*E):
+      * conservation per (k, v): sum_{e out of v} x_ke - sum_{e into v} x_ke = b_kv
+        (equality); commodity k has `terminals` sources and as many sinks with
+        supplies U(1,10), balanced;
+      * joint arc capacity per arc e: 0 <= sum_k x_ke <= cap_e, with
+        cap_e ~ U(1,6) on the random arcs (tight: they bind) and the total
+        demand on the cycle arcs (so the cycle alone routes everything: the LP
+        is feasible);
+      * node inflow capacity per node v: 0 <= sum_k sum_{e into v} x_ke <= ncap_v,
+        ncap_v = U(1,2) * total demand.
+    Costs: U(1,10) per arc, the cycle arcs U(20,40) (expensive detour).
+    All rows are equalities or finite two-sided ranges.
+    The CSR is built directly from the per-commodity pattern (no global sort).
+    """
     rng = np.random.default_rng(seed)
     perm = rng.permutation(V)
     tail = np.concatenate([perm, rng.integers(0, V, E - V)])
     head = np.concatenate([np.roll(perm, -1), rng.integers(0, V, E - V)])
     same = tail == head
     head[same] = (head[same] + 1) % V
-    cost = rng.uniform(1.0, 10.0, E)
-    # each commodity: one source/sink pair with demand d_k routed along
-    src = rng.integers(0, V, K)
-    dst = (src + 1 + rng.integers(0, V - 1, K)) % V
-    dem = rng.uniform(1.0, 10.0, K)
-    cap = rng.uniform(1.0, 2.0, E) * dem.sum()  # the Hamiltonian cycle alone is feasible
+    cyc = np.zeros(E, dtype=bool)
+    cyc[:V] = True
+    cost = np.where(cyc, rng.uniform(20.0, 40.0, E), rng.uniform(1.0, 10.0, E))
+    # supplies: per commodity `terminals` distinct sources and sinks
+    b = np.zeros((K, V))
+    for k in range(K):
+        nodes = rng.choice(V, 2 * terminals, replace=False)
+        s = rng.uniform(1.0, 10.0, terminals)
+        d = rng.uniform(1.0, 10.0, terminals)
+        d *= s.sum() / d.sum()
+        b[k, nodes[:terminals]] += s
+        b[k, nodes[terminals:]] -= d
+    total = float(np.abs(b).sum()) / 2.0
+    cap = np.where(cyc, total, rng.uniform(1.0, 6.0, E))
+    ncap = rng.uniform(1.0, 2.0, V) * total
     n = K * E
     m1 = K * V
-    m = m1 + E
-    k_of = np.repeat(np.arange(K, dtype=np.int64), E)
-    e_of = np.tile(np.arange(E, dtype=np.int64), K)
-    var = np.arange(n, dtype=np.int64)
-    rows = np.concatenate([k_of * V + tail[e_of], k_of * V + head[e_of], m1 + e_of])
-    cols = np.concatenate([var, var, var])
-    vals = np.concatenate([np.ones(n), -np.ones(n), np.ones(n)])
-    rp, ci, v = _csr_from_rows(m, n, rows, cols, vals)
-    b = np.zeros(m1)
-    b[np.arange(K) * V + src] += dem
-    b[np.arange(K) * V + dst] -= dem
-    con_lb = np.concatenate([b, np.zeros(E)])
-    con_ub = np.concatenate([b, cap])
+    m = m1 + E + V
+    # base conservation pattern (commodity 0): row v holds +1 at its out-arcs
+    # and -1 at its in-arcs, columns ascending
+    br = np.concatenate([tail, head]).astype(np.int64)
+    bc = np.concatenate([np.arange(E), np.arange(E)]).astype(np.int64)
+    bv = np.concatenate([np.ones(E), -np.ones(E)])
+    order = np.lexsort((bc, br))
+    br, bc, bv = br[order], bc[order], bv[order]
+    blen = np.bincount(br, minlength=V).astype(np.int64)
+    # node inflow pattern (commodity 0): row v holds its in-arcs ascending
+    ir = head.astype(np.int64)
+    ic = np.arange(E, dtype=np.int64)
+    o2 = np.lexsort((ic, ir))
+    ic = ic[o2]
+    ilen = np.bincount(ir, minlength=V).astype(np.int64)
+    nnz = 2 * E * K + E * K + E * K
+    lens = np.concatenate([np.tile(blen, K), np.full(E, K, dtype=np.int64), ilen * K])
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    assert rp[-1] == nnz
+    ci = np.empty(nnz, dtype=np.int64)
+    v = np.empty(nnz, dtype=np.float64)
+    for k in range(K):  # conservation block of commodity k
+        lo = 2 * E * k
+        ci[lo:lo + 2 * E] = bc + k * E
+        v[lo:lo + 2 * E] = bv
+    lo = 2 * E * K  # arc capacity rows: columns e, E+e, ..., (K-1)E+e
+    ci[lo:lo + E * K] = (np.arange(E, dtype=np.int64)[:, None] +
+                         E * np.arange(K, dtype=np.int64)[None, :]).ravel()
+    v[lo:lo + E * K] = 1.0
+    lo += E * K  # node inflow rows: for k: in-arcs of v shifted by k*E
+    istart = np.zeros(V + 1, dtype=np.int64)
+    np.cumsum(ilen, out=istart[1:])
+    # element j of node row v (length ilen[v]*K): k = j // ilen[v], arc = ic[istart[v] + j % ilen[v]]
+    rows = np.repeat(np.arange(V, dtype=np.int64), ilen * K)
+    j = np.arange(E * K, dtype=np.int64) - np.repeat(istart[:-1] * K, ilen * K)
+    L = ilen[rows]
+    ci[lo:] = ic[istart[rows] + j % L] + (j // L) * E
+    v[lo:] = 1.0
+    del rows, j, L
+    con_lb = np.concatenate([b.ravel(), np.zeros(E), np.zeros(V)])
+    con_ub = np.concatenate([b.ravel(), cap, ncap])
     c = np.tile(cost, K)
     return LpProblem(m, n, rp, ci, v, c, np.zeros(n), np.full(n, INF), con_lb, con_ub,
                      name="c4_multicommodity")

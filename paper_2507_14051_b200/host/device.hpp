@@ -2,6 +2,8 @@
 // that turns status codes back into the rhpdhg exception types.
 #pragma once
 
+#include <memory>
+#include <mutex>
 #include <string>
 
 #include "rhpdhg/errors.hpp"
@@ -87,5 +89,17 @@ inline rhp_options options(const DeviceOptionsT& d) {
   }
   return o;
 }
+
+// A SparseMatrix's cached product context (sparse_matrix.hpp dev_): built on
+// first use from the matrix's CSR (and CSC values when they were set
+// explicitly), with zero objective/bounds; the per-op API uploads the
+// vectors it needs with each call. `mu` serialises its users.
+struct DeviceCache {
+  std::mutex mu;
+  std::unique_ptr<Device> dev;
+};
+
+// Locks the matrix's cache and returns its context (created on first use).
+rhp_ctx* product_context(const SparseMatrix& a, std::unique_lock<std::mutex>& lock);
 
 }  // namespace rhpdhg::detail

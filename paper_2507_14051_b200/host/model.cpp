@@ -126,25 +126,75 @@ const SparseMatrix::Csc& SparseMatrix::csc() const {
   return *csc_;
 }
 
+namespace detail {
+
+DeviceCache& device_cache(const SparseMatrix& a) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!a.dev_) a.dev_ = std::make_shared<DeviceCache>();
+  return *a.dev_;
+}
+
+rhp_ctx* product_context(const SparseMatrix& a, std::unique_lock<std::mutex>& lock) {
+  DeviceCache& cache = device_cache(a);
+  lock = std::unique_lock<std::mutex>(cache.mu);
+  if (!cache.dev) {
+    rhpdhg_lp_view v{};
+    v.num_cons = a.rows();
+    v.num_vars = a.cols();
+    v.nnz = a.nnz();
+    v.row_ptr = a.row_ptr().data();
+    v.col_index = a.col_index().data();
+    v.values = a.csr_values().data();
+    std::vector<double> zn(static_cast<size_t>(a.cols()), 0.0), zm(static_cast<size_t>(a.rows()), 0.0);
+    v.objective = zn.data();
+    v.var_lb = zn.data();
+    v.var_ub = zn.data();
+    v.con_lb = zm.data();
+    v.con_ub = zm.data();
+    const DeviceOptions& d = default_device_options();
+    auto dev = std::make_unique<Device>(v, options(d.device, false, 1));
+    // a scaled matrix's CSC values are scaled from its own CSC values
+    // (sparse_matrix.cpp:101-114), not copies of the CSR ones
+    if (const std::vector<double>* csc = own_csc_values(a); csc && a.nnz() > 0)
+      ok(rhp_set_csc_values(dev->get(), csc->data(), 0), "rhp_set_csc_values");
+    cache.dev = std::move(dev);
+  }
+  return cache.dev->get();
+}
+
+const std::vector<double>* own_csc_values(const SparseMatrix& a) {
+  return (a.csc_ && a.csc_->own_values) ? &a.csc_->val : nullptr;
+}
+
+SparseMatrix with_values(const SparseMatrix& pattern, std::vector<double> csr_values,
+                         std::vector<double> csc_values) {
+  if (csr_values.size() != pattern.val_csr_.size() || csc_values.size() != pattern.val_csr_.size())
+    throw UsageError("with_values: value count does not match the pattern");
+  SparseMatrix r;
+  r.rows_ = pattern.rows_;
+  r.cols_ = pattern.cols_;
+  r.row_ptr_ = pattern.row_ptr_;
+  r.col_idx_ = pattern.col_idx_;
+  r.val_csr_ = std::move(csr_values);
+  const SparseMatrix::Csc& c = pattern.csc();
+  auto rc = std::make_shared<SparseMatrix::Csc>();
+  rc->col_ptr = c.col_ptr;
+  rc->row_idx = c.row_idx;
+  rc->val = std::move(csc_values);
+  rc->own_values = true;
+  r.csc_ = std::move(rc);
+  return r;
+}
+
+}  // namespace detail
+
 namespace {
 void device_product(const SparseMatrix& a, bool transpose, std::span<const double> in,
                     std::span<double> out) {
-  rhpdhg_lp_view v{};
-  v.num_cons = a.rows();
-  v.num_vars = a.cols();
-  v.nnz = a.nnz();
-  v.row_ptr = a.row_ptr().data();
-  v.col_index = a.col_index().data();
-  v.values = a.csr_values().data();
-  std::vector<double> zn(static_cast<size_t>(a.cols()), 0.0), zm(static_cast<size_t>(a.rows()), 0.0);
-  v.objective = zn.data();
-  v.var_lb = zn.data();
-  v.var_ub = zn.data();
-  v.con_lb = zm.data();
-  v.con_ub = zm.data();
-  const DeviceOptions& d = default_device_options();
-  detail::Device dev(v, detail::options(d.device, false, 1));
-  detail::ok(rhp_spmv(dev.get(), transpose ? 1 : 0, in.data(), out.data()), "rhp_spmv");
+  std::unique_lock<std::mutex> lock;
+  rhp_ctx* ctx = detail::product_context(a, lock);
+  detail::ok(rhp_spmv(ctx, transpose ? 1 : 0, in.data(), out.data()), "rhp_spmv");
 }
 }  // namespace
 
@@ -190,7 +240,9 @@ SparseMatrix SparseMatrix::scaled(std::span<const double> row_scale,
   for (Index j = 0; j < cols_; ++j)
     for (Index e = c.col_ptr[j]; e < c.col_ptr[j + 1]; ++e)
       rc->val[e] = col_scale[j] * c.val[e] * row_scale[c.row_idx[e]];
+  rc->own_values = true;
   r.csc_ = std::move(rc);
+  r.dev_.reset();  // new values: its own product context
   return r;
 }
 

@@ -335,17 +335,14 @@ double default_stepsize(double norm_estimate, double multiplier) {
 
 PowerIterationResult power_iteration_norm(const SparseMatrix& matrix, double tol, long max_iters,
                                           std::uint64_t seed) {
-  LpProblem p;
-  p.matrix = matrix;
-  p.objective.assign(static_cast<size_t>(matrix.cols()), 0.0);
-  p.var_lb.assign(static_cast<size_t>(matrix.cols()), 0.0);
-  p.var_ub.assign(static_cast<size_t>(matrix.cols()), 0.0);
-  p.con_lb.assign(static_cast<size_t>(matrix.rows()), 0.0);
-  p.con_ub.assign(static_cast<size_t>(matrix.rows()), 0.0);
-  const DeviceOptions& d = default_device_options();
-  detail::Device dev(detail::view_of(p), detail::options(d.device, false, 1));
-  const PowerIterationResult r =
-      device_power_iteration(dev.get(), matrix.cols(), matrix.nnz(), tol, max_iters, seed);
+  PowerIterationResult r;
+  if (matrix.nnz() == 0) {
+    r.converged = true;
+  } else {  // on the matrix's cached product context
+    std::unique_lock<std::mutex> lock;
+    rhp_ctx* ctx = detail::product_context(matrix, lock);
+    r = device_power_iteration(ctx, matrix.cols(), matrix.nnz(), tol, max_iters, seed);
+  }
   spmv_counter::add(2u * static_cast<std::uint64_t>(r.iterations));
   return r;
 }
@@ -405,35 +402,10 @@ ScalingInfo ScalingInfo::identity(const LpProblem& p) {
 
 std::pair<LpProblem, ScalingInfo> scale_problem(const LpProblem& problem, bool enabled,
                                                 int ruiz_iterations, bool pock_chambolle) {
-  problem.validate();
-  const DeviceOptions& d = default_device_options();
-  detail::Device dev(detail::view_of(problem), detail::options(d.device, false, 1));
-  detail::ok(rhp_scale(dev.get(), enabled ? 1 : 0, ruiz_iterations, pock_chambolle ? 1 : 0), "rhp_scale");
-  const size_t m = static_cast<size_t>(problem.num_cons()), n = static_cast<size_t>(problem.num_vars());
-  std::vector<double> vals(static_cast<size_t>(problem.matrix.nnz()));
-  LpProblem out;
-  out.name = problem.name;
-  out.maximization = problem.maximization;
-  out.objective_offset = problem.objective_offset;
-  out.objective.resize(n);
-  out.var_lb.resize(n);
-  out.var_ub.resize(n);
-  out.con_lb.resize(m);
-  out.con_ub.resize(m);
-  ScalingInfo info;
-  info.row_scale.resize(m);
-  info.col_scale.resize(n);
-  info.active = enabled;
-  rhp_scaled_out o{vals.data(), nullptr, info.row_scale.data(), info.col_scale.data(),
-                   out.objective.data(), out.var_lb.data(), out.var_ub.data(),
-                   out.con_lb.data(), out.con_ub.data()};
-  detail::ok(rhp_get_scaled(dev.get(), &o), "rhp_get_scaled");
-  const auto rp = problem.matrix.row_ptr();
-  const auto ci = problem.matrix.col_index();
-  out.matrix = SparseMatrix::from_csr(problem.num_cons(), problem.num_vars(),
-                                      std::vector<Index>(rp.begin(), rp.end()),
-                                      std::vector<Index>(ci.begin(), ci.end()), std::move(vals));
-  return {std::move(out), std::move(info)};
+  if (!enabled) return {problem, ScalingInfo::identity(problem)};  // solver.cpp:72-78
+  auto [scaled, info] = ruiz_equilibrate(problem, ruiz_iterations);
+  if (pock_chambolle) scaled = pock_chambolle_scale(scaled, info);
+  return {std::move(scaled), std::move(info)};
 }
 
 }  // namespace rhpdhg

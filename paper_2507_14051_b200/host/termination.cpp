@@ -90,11 +90,21 @@ KktResiduals kkt_residuals(const LpProblem& p, std::span<const double> x,
                            std::span<const double> y) {
   if (static_cast<Index>(x.size()) != p.num_vars() || static_cast<Index>(y.size()) != p.num_cons())
     throw UsageError("kkt_residuals: size mismatch");
+  if (static_cast<Index>(p.objective.size()) != p.num_vars() ||
+      static_cast<Index>(p.var_lb.size()) != p.num_vars() ||
+      static_cast<Index>(p.var_ub.size()) != p.num_vars() ||
+      static_cast<Index>(p.con_lb.size()) != p.num_cons() ||
+      static_cast<Index>(p.con_ub.size()) != p.num_cons())
+    throw UsageError("kkt_residuals: problem vector sizes do not match the matrix");
   spmv_counter::add(2);
-  const DeviceOptions& d = default_device_options();
-  detail::Device dev(detail::view_of(p), detail::options(d.device, false, 1));
+  // on the matrix's cached product context, with this problem's vectors
+  std::unique_lock<std::mutex> lock;
+  rhp_ctx* ctx = detail::product_context(p.matrix, lock);
+  const rhp_op_lp vec{p.objective.data(), p.var_lb.data(), p.var_ub.data(), p.con_lb.data(),
+                      p.con_ub.data()};
+  detail::ok(rhp_set_vectors(ctx, &vec), "rhp_set_vectors");
   rhp_kkt_sums s{};
-  detail::ok(rhp_kkt_of(dev.get(), x.data(), y.data(), &s), "rhp_kkt_of");
+  detail::ok(rhp_kkt_of(ctx, x.data(), y.data(), &s), "rhp_kkt_of");
   return detail::residuals_from_sums(s, detail::problem_denoms(p));
 }
 

@@ -1,11 +1,14 @@
 """Benchmark of the restarted reflected-Halpern PDHG hot path (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
-                    [--config c2] [--no-e2e] [--no-cpu-baseline]
+                    [--config c1..c5] [--no-e2e] [--no-cpu-baseline] [--no-parity]
 
-Workload: BASELINE.json configs[1] (C2: synthetic MIPLIB-relaxation-like LP,
-m=500k, n=1M, ~10M nnz, power-law row lengths), generated on the host from a
-fixed seed (data "synthetic"). All arithmetic is fp64.
+Workload (N = 1): BASELINE.json configs[3], C4 — the largest single-GPU
+configuration and the one the north star's ">= 50x time-to-1e-8" target is
+quoted on: a synthetic multicommodity-flow LP with 100M nonzeros (K = 25
+commodities, n = 25M, m = 6.2M, binding arc capacities), generated on the host
+from a fixed seed (data "synthetic"). N > 1: C5 (~1B nonzeros,
+row-partitioned over the N GPUs). All arithmetic is fp64.
 
 A "step" = one KKT check interval of the solve loop: 64 restarted reflected
 Halpern PDHG iterations (each: A x+, A^T y+ and the fused primal / dual /
@@ -13,15 +16,19 @@ Halpern / reflection updates and residual reductions) plus the KKT check and
 any restarts they trigger, run through the product's resumable C-ABI session
 (include/rhpdhg_c.h). `value` is PDHG iterations/s with the LP resident in
 HBM, timed with CUDA events on the solve's stream around exactly K steps
-(the matrix, ~240 MB, is larger than L2, so no flush is needed); `e2e` is the
-same metric through rhpdhg_session_create/finish with HOST buffers: upload,
-scaling, power iteration, the solve to 1e-8 relative KKT and the download of
-the solution are inside the timed region.
+(the matrices, 24 B/nnz, are larger than L2, so no flush is needed); `e2e`
+is the same metric through rhpdhg_session_create/advance/finish with HOST
+buffers: upload, scaling, power iteration, the solve to 1e-8 relative KKT and
+the download of the solution are inside the timed region. `parity` (outside
+every timed region) re-checks the e2e solution with the oracle's independent
+KKT evaluation and compares the first iterates with the oracle.
+
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under `torch.distributed.run` with N processes (one per GPU).
 
 --impl reference times the reference's own CPU implementation (the
 unmodified reference library compiled from /root/reference into
-oracle/_ref, single-threaded as shipped) on the same LP, K steps of 8
-iterations each after its setup.
+oracle/_ref, single-threaded as shipped) on the same LP; see run_reference.
 """
 from __future__ import annotations
 
@@ -112,12 +119,12 @@ class ClockSampler:
 
 # ------------------------------------------------------------ distributed ----
 class Dist:
-    def __init__(self):
+    def __init__(self, init_nccl=True):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.torch = None
-        if self.world > 1:
+        if self.world > 1 and init_nccl:
             import torch
             import torch.distributed as dist
 
@@ -180,24 +187,45 @@ WORKLOADS = {
           "E=1M, n=25M, m=6.2M, 100M nnz; binding arc capacities + node capacities)",
     "c5": "C5 synthetic row-partitionable LP (m=50M, n=20M, ~1B nnz, power-law rows)",
 }
-# C5's CPU sample: the reference on the same generator at 1/50 scale (20M
-# nonzeros), per-iteration and setup cost extrapolated linearly in nonzeros
+# Bounded CPU samples of the configurations whose reference setup alone runs
+# for minutes on one core (C4: ~400 s, C5: hours): the reference's loop is
+# timed on the full LP after an abbreviated setup (no Ruiz / Pock-Chambolle
+# passes, power iteration capped at 5 products: the loop's per-iteration
+# work does not depend on either), and its full setup is measured on a
+# reduced instance of the same generator and extrapolated linearly in nnz.
+BOUNDED = {"c4", "c5"}
+SETUP_SAMPLE = {"c4": dict(V=20_000, E=100_000, K=25), "c5": dict(m=1_000_000, n=400_000)}
+# C5 (1B nonzeros, ~16 GB of host CSR) is sampled whole at 1/50 scale
 C5_CPU_SAMPLE = dict(m=1_000_000, n=400_000)
 
 
+def host_cpu():
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count(),
+            "cores_used": 1, "note": "the reference is single-threaded as shipped (no threads, "
+                                     "OpenMP or SIMD intrinsics): 1 core is its full speed"}
+
+
 # --------------------------------------------------------------- CPU arm -----
-def cpu_sample(lp, iters, label):
-    """Reference (oracle/_ref) when built, else the oracle port; 1 core."""
+def fast_cfg():
+    """Abbreviated-setup config for timing the reference's loop (see BOUNDED)."""
+    return SolverConfig(epsilon=1e-300, ruiz_iterations=0, pock_chambolle=False,
+                        power_max_iters=5)
+
+
+def cpu_sample(lp, iters, label, config):
+    """The reference (oracle/_ref) when built, else the oracle port; 1 core."""
     sys.path.insert(0, str(ROOT / "tests"))
     import support
 
-    if support.ref_available():
-        s = support.RefSession(lp, SolverConfig(epsilon=1e-300))
-        setup = s.setup_seconds
-        _, secs, total = s.advance(iters)
-        s.close()
-        kind = "reference"
-    else:
+    if not support.ref_available():
         o = support.oracle()
         t0 = time.perf_counter()
         support.solve_with(o, lp, SolverConfig(epsilon=1e-300, iteration_limit=0))
@@ -205,52 +233,130 @@ def cpu_sample(lp, iters, label):
         t0 = time.perf_counter()
         support.solve_with(o, lp, SolverConfig(epsilon=1e-300, iteration_limit=iters))
         secs = time.perf_counter() - t0 - setup
-        total = iters
-        kind = "port"
-    return {"value": total / secs, "unit": UNIT, "cores": 1, "kind": kind,
+        return {"value": iters / secs, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"{label}: oracle port, setup {setup:.1f} s then {iters} iterations "
+                          f"({secs:.1f} s), 1 thread", "setup_seconds": setup,
+                "loop_seconds": secs, "iterations": iters, **host_cpu()}
+    if config in BOUNDED:
+        s = support.RefSession(lp, fast_cfg())
+        _, secs, total = s.advance(iters)
+        s.close()
+        small = generators.CONFIGS[config](**SETUP_SAMPLE[config])
+        ss = support.RefSession(small, SolverConfig(epsilon=1e-300))
+        ratio = lp.nnz / small.nnz
+        setup = ss.setup_seconds * ratio
+        small_setup = ss.setup_seconds
+        ss.close()
+        return {"value": total / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"{label}: the reference's loop on this LP, {total} iterations "
+                          f"({secs:.1f} s, 1 thread) after an abbreviated setup (no scaling "
+                          f"passes, power iteration capped at 5); its full setup (Ruiz + "
+                          f"Pock-Chambolle + power iteration) measured on the same generator at "
+                          f"{small.nnz} nnz ({small_setup:.1f} s) and extrapolated x{ratio:.1f}",
+                "setup_seconds": setup, "setup_extrapolated": True, "loop_seconds": secs,
+                "iterations": total, **host_cpu()}
+    s = support.RefSession(lp, SolverConfig(epsilon=1e-300))
+    setup = s.setup_seconds
+    _, secs, total = s.advance(iters)
+    s.close()
+    return {"value": total / secs, "unit": UNIT, "cores": 1, "kind": "reference",
             "sample": f"{label}: setup (Ruiz+Pock-Chambolle+power iteration, {setup:.1f} s) then "
                       f"{total} loop iterations incl. KKT checks ({secs:.1f} s), 1 thread",
-            "setup_seconds": setup, "loop_seconds": secs, "iterations": total}
+            "setup_seconds": setup, "loop_seconds": secs, "iterations": total, **host_cpu()}
 
 
 def run_reference(args):
-    dist = Dist()
+    dist = Dist(init_nccl=False)
     if dist.rank != 0:
-        dist.close()
         return 0
     sys.path.insert(0, str(ROOT / "tests"))
     import support
 
-    lp, _ = make_lp(args.config)
-    cfg_run = {"workload": WORKLOADS[args.config], "m": lp.num_cons, "n": lp.num_vars,
-               "nnz": lp.nnz, "parallelism": "1 CPU thread (reference is single-threaded)"}
     if not support.ref_available():
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref not built (needs /root/reference at build time)"}))
         return 0
-    s = support.RefSession(lp, SolverConfig(epsilon=1e-300))
-    per_step = args.ref_step_iters
+    if args.config == "c5":
+        lp = generators.c5_rowpart(**C5_CPU_SAMPLE, device="cpu")
+        scale = generators_nnz_c5() / lp.nnz
+        sample = (f"the reference on the C5 generator at m={lp.num_cons}, n={lp.num_vars}, "
+                  f"{lp.nnz} nnz, iter/s scaled by 1/{scale:.1f} (linear in nnz)")
+    else:
+        lp, _ = make_lp(args.config)
+        scale = 1.0
+        sample = "the reference's loop on the full LP"
+    cfg_run = {"workload": WORKLOADS[args.config], "m": lp.num_cons, "n": lp.num_vars,
+               "nnz": lp.nnz, "parallelism": "1 CPU thread (reference is single-threaded)"}
+    bounded = args.config in BOUNDED
+    s = support.RefSession(lp, fast_cfg() if bounded else SolverConfig(epsilon=1e-300))
+    per_step = args.ref_step_iters if args.ref_step_iters else (1 if bounded else 8)
     for _ in range(args.warmup):
         s.advance(per_step)
     t0 = time.perf_counter()
     total = 0
     for _ in range(args.steps):
-        _, _, _ = s.advance(per_step)
+        s.advance(per_step)
         total += per_step
     secs = time.perf_counter() - t0
     s.close()
-    v = total / secs
+    v = total / secs / scale
+    if bounded:
+        sample += (" after an abbreviated setup (no Ruiz / Pock-Chambolle passes, power "
+                   "iteration capped at 5: the per-iteration work does not depend on either)")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / args.steps * scale,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": dict(cfg_run, step=f"{per_step} PDHG iterations"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
-                             "sample": f"{args.steps} steps x {per_step} iterations after "
-                                       f"{s.setup_seconds:.1f} s setup"},
+                             "sample": f"{args.steps} steps x {per_step} iterations: {sample}",
+                             **host_cpu()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "setup_seconds": s.setup_seconds}
     print(json.dumps(line))
     return 0
+
+
+def generators_nnz_c5():
+    """Expected nnz of the full C5 (mean row length 20 x 50M rows)."""
+    return 50_000_000 * 20
+
+
+# ------------------------------------------------------------------ parity ---
+def parity_block(lp, config, e2e_x, e2e_y, e2e_tol):
+    """Outside every timed region: (1) the e2e solution re-checked by the
+    oracle's independent kkt_residuals; (2) the product's first iterates
+    (k = 1, 10) against the oracle's (orc_solve_snapshots). The full parity
+    suite at bench size is tests/test_bench_parity.py."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import support
+    from paper_2507_14051_b200.lp import solve
+
+    out = {"suite": "tests/test_bench_parity.py (first iterates k=1,10,64,65,100 vs the "
+                    "reference / oracle, objective at 1e-4 vs the reference, oracle KKT at 1e-8)"}
+    t0 = time.perf_counter()
+    if e2e_x is not None:
+        r = support.kkt_with(support.oracle(), lp, e2e_x, e2e_y)
+        ok = (r["gap_rel"] <= e2e_tol and r["primal_rel"] <= e2e_tol and
+              r["dual_eq"] <= e2e_tol * r["dual_denom"] and
+              r["dual_cone"] <= e2e_tol * r["dual_denom"])
+        out["oracle_kkt"] = {"tol": e2e_tol, "optimal": ok, "gap_rel": r["gap_rel"],
+                             "primal_rel": r["primal_rel"],
+                             "dual_rel": r["dual_eq"] / r["dual_denom"]}
+    ks = [1, 10]
+    xs, ys = support.oracle_snapshots(lp, SolverConfig(epsilon=1e-300, iteration_limit=max(ks)),
+                                      ks)
+    devs = []
+    for i, k in enumerate(ks):
+        rep = solve(lp, SolverConfig(epsilon=1e-300, iteration_limit=k))
+        dx = float(np.max(np.abs(np.asarray(rep.x) - xs[i])) / max(np.max(np.abs(xs[i])), 1e-300))
+        dy = float(np.max(np.abs(np.asarray(rep.y) - ys[i])) / max(np.max(np.abs(ys[i])), 1e-300))
+        devs.append(max(dx, dy))
+    out["first_iterates"] = {"k": ks, "max_rel_dev": devs, "tol": 1e-10,
+                             "checker": "oracle (bit-identical to the reference on the golden set)",
+                             "pass": max(devs) <= 1e-10}
+    out["seconds"] = time.perf_counter() - t0
+    return out
 
 
 # ---------------------------------------------------------------- GPU arm ----
@@ -358,6 +464,7 @@ def run_product(args):
 
     # ---- e2e through the C ABI with host buffers, to 1e-8 (cap)
     e2e = None
+    e2e_sol = None
     if not args.no_e2e:
         dist.barrier()
         t0 = time.perf_counter()
@@ -375,6 +482,7 @@ def run_product(args):
                     it_1e4 = s2.info()["total"]
         rep = s2.finish()
         t_e2e = time.perf_counter() - t0
+        e2e_sol = (np.asarray(rep.x), np.asarray(rep.y))
         s2.close()
         t_e2e_max = dist.max(t_e2e)
         e2e = {"value": rep.iterations / t_e2e_max, "unit": UNIT,
@@ -392,7 +500,7 @@ def run_product(args):
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
         if args.config == "c5":
             small = generators.c5_rowpart(**C5_CPU_SAMPLE)
-            cpu = cpu_sample(small, args.cpu_iters, "C5 generator at 1/50 scale")
+            cpu = cpu_sample(small, args.cpu_iters, "C5 generator at 1/50 scale", "c2")
             ratio = lp.nnz / small.nnz
             cpu["value"] /= ratio
             cpu["setup_seconds"] *= ratio
@@ -401,7 +509,8 @@ def run_product(args):
                              f"iterations, 1 thread); iter/s and setup extrapolated linearly in "
                              f"nonzeros (x{ratio:.1f})")
         else:
-            cpu = cpu_sample(lp, args.cpu_iters, WORKLOADS[args.config])
+            iters = args.cpu_iters if args.cpu_iters else (8 if args.config in BOUNDED else 64)
+            cpu = cpu_sample(lp, iters, WORKLOADS[args.config], args.config)
         if e2e and e2e["status"] == "optimal":
             it = e2e["iterations"]
             cpu["time_to_tol_extrapolated_s"] = cpu["setup_seconds"] + it / cpu["value"]
@@ -410,6 +519,12 @@ def run_product(args):
             if e2e.get("iterations_to_1e-4"):
                 cpu["time_to_1e-4_extrapolated_s"] = (cpu["setup_seconds"] +
                                                       e2e["iterations_to_1e-4"] / cpu["value"])
+            cpu["time_to_tol_speedup_vs_e2e"] = cpu["time_to_tol_extrapolated_s"] / e2e["time_to_tol_s"]
+
+    parity = None
+    if not args.no_parity and dist.rank == 0 and dist.world == 1 and args.config != "c5":
+        parity = parity_block(lp, args.config, e2e_sol[0] if e2e_sol else None,
+                              e2e_sol[1] if e2e_sol else None, args.e2e_eps)
 
     if dist.rank == 0:
         line = {
@@ -428,7 +543,7 @@ def run_product(args):
                        "setup_s": info0["setup_seconds"]},
             "roofline": roofline, "clocks": clk, "gpu_launches": launches,
             "timed_iterations": iters, "restarts_in_timed": b["restarts"] - a["restarts"],
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         }
         if e2e:
             line["time_to_1e-8_s"] = e2e["time_to_tol_s"] if args.e2e_eps == 1e-8 else None
@@ -438,25 +553,54 @@ def run_product(args):
     return 0
 
 
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script as N ranks."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(generators.CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(generators.CONFIGS),
+                    help="default: c4 at one GPU, c5 (row-partitioned) at N > 1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=64)
-    ap.add_argument("--ref-step-iters", type=int, default=8)
+    ap.add_argument("--cpu-iters", type=int, default=0,
+                    help="reference loop iterations of the cpu_baseline sample "
+                         "(default 8 for c4/c5, else 64)")
+    ap.add_argument("--ref-step-iters", type=int, default=0,
+                    help="iterations per --impl reference step (default 1 for c4/c5, else 8)")
     ap.add_argument("--e2e-eps", type=float, default=1e-8)
-    # C2 needs ~404k iterations to 1e-8 (~80 s on one B200)
-    ap.add_argument("--e2e-cap", type=int, default=600_000)
+    # C2 needs ~404k iterations to 1e-8 (~60 s on one B200); C4 ~56k
+    ap.add_argument("--e2e-cap", type=int, default=0,
+                    help="iteration cap of the e2e solve (default 600k; c5: 2048, since "
+                         "1e-4 takes > 150k iterations there)")
     ap.add_argument("--profile-kernels", type=int, default=0,
                     help="profiling mode: after warmup, launch K3/K1/K2 N times each inside "
                          "a cudaProfilerStart/Stop range and exit")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "c4" if args.gpus == 1 else "c5"
+    if not args.e2e_cap:
+        args.e2e_cap = 2048 if args.config == "c5" else 600_000
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_product(args)

@@ -13,8 +13,9 @@
 //   ref_power_iteration    -> power_iteration_norm          (pdhg.cpp:117-170)
 //   ref_lp_from_mps        -> parse_mps_file                (mps.cpp:417-435)
 //   ref_lp_random_feasible -> testutil::random_feasible_lp  (tests/oracles.hpp:61-110)
-//   ref_bench_sample       -> setup + N loop iterations through the public
-//                             per-op API (restart.hpp:47-70), timed.
+//   ref_session_*          -> setup + N loop iterations through the public
+//                             per-op API (restart.hpp:47-70), timed; the
+//                             current iterate in original space.
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -357,6 +358,17 @@ int ref_session_advance(void* hv, int64_t iters, int32_t* running, double* secon
 }
 
 double ref_session_setup_seconds(void* hv) { return static_cast<RefSession*>(hv)->setup_seconds; }
+
+// The current Halpern iterate in original space (unscale_iterate,
+// scaling.cpp:83-94): what solve() reports for x, y after `total` iterations.
+int ref_session_iterate(void* hv, double* x, double* y) {
+  return guarded([&] {
+    RefSession& h = *static_cast<RefSession*>(hv);
+    const Iterate o = unscale_iterate(h.z, h.info);
+    std::copy(o.x.begin(), o.x.end(), x);
+    std::copy(o.y.begin(), o.y.end(), y);
+  });
+}
 
 void ref_session_free(void* hv) { delete static_cast<RefSession*>(hv); }
 

@@ -88,8 +88,11 @@ static int mat_from_view(const rhpdhg_lp_view* lp, Mat* a) {
   return 0;
 }
 
-/* out = A x, sequential row sums (sparse_matrix.cpp:67-76). */
+/* out = A x, sequential row sums (sparse_matrix.cpp:67-76). Rows are
+ * independent, so the OpenMP row split (bench-size parity tests) leaves every
+ * row sum, and so every result, bit-identical to the sequential loop. */
 static void mat_mul(const Mat* a, const double* x, double* out) {
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t i = 0; i < a->m; ++i) {
     double acc = 0.0;
     for (int64_t e = a->rp[i]; e < a->rp[i + 1]; ++e) acc += a->v[e] * x[a->ci[e]];
@@ -99,6 +102,7 @@ static void mat_mul(const Mat* a, const double* x, double* out) {
 
 /* out = A^T y over the CSC copy (sparse_matrix.cpp:78-87). */
 static void mat_mul_t(const Mat* a, const double* y, double* out) {
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t j = 0; j < a->n; ++j) {
     double acc = 0.0;
     for (int64_t e = a->cp[j]; e < a->cp[j + 1]; ++e) acc += a->vt[e] * y[a->ri[e]];
@@ -110,8 +114,10 @@ static void mat_mul_t(const Mat* a, const double* y, double* out) {
  * CSR (r_i a) c_j, CSC (c_j a) r_i (sparse_matrix.cpp:101-114). Both copies
  * are rebuilt from the given (unscaled-by-this-call) values. */
 static void mat_scale(Mat* a, const double* rs, const double* cs) {
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t i = 0; i < a->m; ++i)
     for (int64_t e = a->rp[i]; e < a->rp[i + 1]; ++e) a->v[e] = rs[i] * a->v[e] * cs[a->ci[e]];
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t j = 0; j < a->n; ++j)
     for (int64_t e = a->cp[j]; e < a->cp[j + 1]; ++e) a->vt[e] = cs[j] * a->vt[e] * rs[a->ri[e]];
 }
@@ -529,6 +535,14 @@ static double pid_update(Pid* pid, const It* z, const double* sx, const double* 
   return omega;
 }
 
+/* Snapshot request of orc_solve_snapshots (test infrastructure, one solve at
+ * a time): after the iteration that brings `total` to ks[i], the unscaled
+ * Halpern iterate (x = D_col x_bar, y = D_row y_bar) goes to xs + i*n,
+ * ys + i*m. */
+static const int64_t* g_snap_k = NULL;
+static int g_snap_nk = 0;
+static double *g_snap_x = NULL, *g_snap_y = NULL;
+
 int orc_solve_csr(const rhpdhg_lp_view* lpv, const rhpdhg_config_c* cfg, rhpdhg_report_c* rep,
                   double* x_out, double* y_out, double* rc_out, double* hist, int64_t hist_cap) {
   if (!cfg_ok(cfg)) return fail(RHPDHG_E_USAGE, "invalid solver configuration");
@@ -702,6 +716,11 @@ int orc_solve_csr(const rhpdhg_lp_view* lpv, const rhpdhg_config_c* cfg, rhpdhg_
       r_anchor = INFINITY;
       r_prev = INFINITY;
     }
+    for (int s2 = 0; s2 < g_snap_nk; ++s2)
+      if (g_snap_k[s2] == total) {
+        for (int64_t j = 0; j < n; ++j) g_snap_x[(size_t)s2 * n + j] = cs[j] * z.x[j];
+        for (int64_t i = 0; i < m; ++i) g_snap_y[(size_t)s2 * m + i] = rs[i] * z.y[i];
+      }
   }
   if (status != RHPDHG_OPTIMAL) {
     rc = kkt_check(&z, &orig, rs, cs, xo, yo, axo, atyo, &res);
@@ -741,6 +760,19 @@ done:
   free(sx); free(sy); free(xo); free(yo); free(axo); free(atyo); free(rs); free(cs);
   lp_free(&orig);
   lp_free(&sc);
+  return rc;
+}
+
+int orc_solve_snapshots(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg,
+                        rhpdhg_report_c* rep, const int64_t* ks, int nk, double* xs, double* ys) {
+  g_snap_k = ks;
+  g_snap_nk = nk;
+  g_snap_x = xs;
+  g_snap_y = ys;
+  const int rc = orc_solve_csr(lp, cfg, rep, NULL, NULL, NULL, NULL, 0);
+  g_snap_k = NULL;
+  g_snap_nk = 0;
+  g_snap_x = g_snap_y = NULL;
   return rc;
 }
 

@@ -35,6 +35,12 @@ int orc_solve_csr(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg, rhpdhg_r
                   double* x, double* y, double* reduced_costs, double* history,
                   int64_t history_cap);
 
+/* solve() with iterate snapshots: after the iteration that brings the total
+ * count to ks[i], the unscaled iterate (x, y) is written to xs + i*n,
+ * ys + i*m (the x, y solve() would report with iteration_limit = ks[i]). */
+int orc_solve_snapshots(const rhpdhg_lp_view* lp, const rhpdhg_config_c* cfg,
+                        rhpdhg_report_c* rep, const int64_t* ks, int nk, double* xs, double* ys);
+
 /* SparseMatrix::multiply / multiply_transpose — sparse_matrix.cpp:67-87 */
 int orc_spmv(const rhpdhg_lp_view* lp, const double* in, double* out, int transpose);
 

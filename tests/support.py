@@ -56,6 +56,10 @@ def oracle():
         _type_common(lib, "orc")
         lib.orc_power_start.argtypes = [C.c_int64, C.c_uint64, D]
         lib.orc_power_start.restype = None
+        lib.orc_solve_snapshots.argtypes = [C.POINTER(capi.LpView), C.POINTER(capi.ConfigC),
+                                            C.POINTER(capi.ReportC), capi.c_int64_p, C.c_int,
+                                            D, D]
+        lib.orc_solve_snapshots.restype = C.c_int
         _libs["orc"] = lib
     return _libs["orc"]
 
@@ -90,6 +94,8 @@ def ref():
         lib.ref_session_setup_seconds.restype = C.c_double
         lib.ref_session_free.argtypes = [C.c_void_p]
         lib.ref_session_free.restype = None
+        lib.ref_session_iterate.argtypes = [C.c_void_p, D, D]
+        lib.ref_session_iterate.restype = C.c_int
         _libs["ref"] = lib
     return _libs["ref"]
 
@@ -147,6 +153,23 @@ def kkt_with(lib, lp: LpProblem, x, y):
     return out.as_dict()
 
 
+def oracle_snapshots(lp: LpProblem, cfg: SolverConfig, ks):
+    """Unscaled iterates (x, y) after each iteration count in ks, from ONE
+    oracle solve (orc_solve_snapshots; OpenMP row-parallel products, results
+    bit-identical to the sequential oracle)."""
+    lib = oracle()
+    ks = np.ascontiguousarray(ks, dtype=np.int64)
+    xs = np.zeros((len(ks), lp.num_vars))
+    ys = np.zeros((len(ks), lp.num_cons))
+    view = lp.view()
+    cc = cfg.to_c()
+    rep = capi.ReportC()
+    check(lib, lib.orc_solve_snapshots(C.byref(view), C.byref(cc), C.byref(rep),
+                                       ks.ctypes.data_as(capi.c_int64_p), len(ks),
+                                       xs.ctypes.data_as(D), ys.ctypes.data_as(D)))
+    return xs, ys
+
+
 def ref_lp_from_handle(h) -> LpProblem:
     lib = ref()
     if not h:
@@ -188,6 +211,14 @@ class RefSession:
         check(self.lib, self.lib.ref_session_advance(self.h, iters, C.byref(running),
                                                      C.byref(secs), C.byref(total)))
         return bool(running.value), secs.value, total.value
+
+    def iterate(self):
+        """Current Halpern iterate in original space (x, y)."""
+        x = np.zeros(self._lp.num_vars)
+        y = np.zeros(self._lp.num_cons)
+        check(self.lib, self.lib.ref_session_iterate(self.h, x.ctypes.data_as(D),
+                                                     y.ctypes.data_as(D)))
+        return x, y
 
     def close(self):
         if self.h:

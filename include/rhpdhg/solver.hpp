@@ -26,9 +26,13 @@ struct DeviceOptions {
   int rank = 0;
   int world_size = 1;
   std::vector<char> nccl_id;  // empty: single-GPU path
+  // Instead of NCCL: an in-process collective group (rhp_local_group_create)
+  // shared by world_size threads of this process, one rank each.
+  const void* local_group = nullptr;
 };
 
-/// Process-wide default device options (used by solve(problem, cfg)).
+/// The calling thread's default device options (used by solve(problem, cfg));
+/// per thread so threads of one process can act as different ranks.
 DeviceOptions& default_device_options();
 
 SolutionReport solve(const LpProblem& problem, const SolverConfig& cfg);

@@ -168,6 +168,11 @@ int rhpdhg_set_device_options(int device, int use_graph, int64_t block_limit);
  * 128-byte NCCL unique id (rhp_nccl_unique_id in rhpdhg_cuda.h). nccl_id NULL
  * with world_size 1 restores single-GPU solves. */
 int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id);
+/* Same with an in-process collective group (rhp_local_group_create in
+ * rhpdhg_cuda.h) instead of NCCL: world_size threads of this process, each
+ * calling this with its rank, solve one LP together. Device options are per
+ * thread. */
+int rhpdhg_set_local_group(int rank, int world_size, const void* group);
 /* Small-LP cluster-resident device blocks: -1 auto (default), 0 off, 1 on. */
 int rhpdhg_set_resident(int mode);
 

@@ -59,6 +59,11 @@ typedef struct rhp_options {
   const void* nccl_id;   /* 128 bytes when world_size > 1, else NULL */
   int32_t resident;      /* small-LP cluster-resident blocks: -1 auto, 0 off, 1 on */
   int32_t pad_;
+  /* In-process collective group (rhp_local_group_create) instead of NCCL:
+   * world_size contexts of ONE process, each driven by its own host thread,
+   * exchange through device memory with rank-ordered reductions. Lets the
+   * row-partitioned engine run at world_size > 1 on a single GPU (tests). */
+  const void* local_group;
 } rhp_options;
 
 /* Step and restart parameters of the device loop. Derived quantities are
@@ -148,6 +153,10 @@ int rhp_get_device_info(int device, rhp_device_info* info);
 int rhp_nccl_unique_id(void* out128);
 
 int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt, rhp_ctx** out);
+/* In-process collective group of `world` ranks (see rhp_options.local_group);
+ * destroy only after every context using it. */
+int rhp_local_group_create(int world, void** out);
+int rhp_local_group_destroy(void* group);
 int rhp_destroy(rhp_ctx* ctx);
 int rhp_layout(rhp_ctx* ctx, rhp_layout_info* info);
 

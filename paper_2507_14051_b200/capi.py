@@ -122,6 +122,7 @@ class RhpOptions(C.Structure):
         ("nccl_id", C.c_void_p),
         ("resident", C.c_int32),
         ("pad_", C.c_int32),
+        ("local_group", C.c_void_p),
     ]
 
 
@@ -194,11 +195,12 @@ CUDA_SYMBOLS = [
     "rhp_last_block_ms", "rhp_timer", "rhp_time_kernels", "rhp_time_spmv", "rhp_gather_ceiling", "rhp_profiler_range",
     "rhp_synchronize",
     "rhp_op_pdhg", "rhp_set_vectors", "rhp_set_csc_values", "rhp_op_sums", "rhp_op_mul",
+    "rhp_local_group_create", "rhp_local_group_destroy",
 ]
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",
     "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_set_distributed",
-    "rhpdhg_set_resident",
+    "rhpdhg_set_resident", "rhpdhg_set_local_group",
     "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
@@ -258,6 +260,14 @@ def load_cuda() -> C.CDLL:
             "rhp_time_spmv": [P, C.c_int, C.c_int, c_double_p],
             "rhp_gather_ceiling": [P, C.c_int, c_double_p, c_double_p],
             "rhp_synchronize": [P],
+            "rhp_op_pdhg": [P, P, P, P, P, P, c_double_p, c_double_p, P],
+            "rhp_set_vectors": [P, P],
+            "rhp_set_csc_values": [P, c_double_p, C.c_int],
+            "rhp_op_sums": [C.c_int, C.c_int64, c_double_p, c_double_p, C.c_int64, c_double_p,
+                            c_double_p, c_double_p, c_double_p],
+            "rhp_op_mul": [C.c_int, C.c_int64, c_double_p, c_double_p, c_double_p],
+            "rhp_local_group_create": [C.c_int, C.POINTER(P)],
+            "rhp_local_group_destroy": [P],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)
@@ -287,6 +297,7 @@ def load_host() -> C.CDLL:
         sig = {
             "rhpdhg_set_device_options": [C.c_int, C.c_int, C.c_int64],
             "rhpdhg_set_distributed": [C.c_int, C.c_int, C.c_void_p],
+            "rhpdhg_set_local_group": [C.c_int, C.c_int, C.c_void_p],
             "rhpdhg_set_resident": [C.c_int],
             "rhpdhg_session_create": [C.POINTER(LpView), C.POINTER(ConfigC), C.POINTER(P)],
             "rhpdhg_session_advance": [P, C.c_int64, C.POINTER(C.c_int32)],

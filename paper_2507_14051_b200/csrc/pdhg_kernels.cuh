@@ -235,7 +235,11 @@ struct EpiDual {
 __global__ void __launch_bounds__(kBlock) k_dist_control(Ctl* ctl, const double* part3, int grid3,
                                                          int n_multi3, const double* long_red3,
                                                          const double* xsums, int token) {
-  if (!ctl->graph_mode && ctl->k1_token_pending != token && !ctl->bench) return;
+  if (!ctl->graph_mode && ctl->k1_token_pending != token && !ctl->bench) {
+    // an iteration past the block's stop: tell the host (rhp_run_block polls)
+    if (threadIdx.x == 0 && ctl->stop_mirror) reinterpret_cast<volatile int*>(ctl->stop_mirror)[token] = 1;
+    return;
+  }
   double t3[4];
   block_sum_partials<4>(part3, grid3, grid3, t3);
   add_slots<4>(long_red3, n_multi3, t3);
@@ -243,6 +247,7 @@ __global__ void __launch_bounds__(kBlock) k_dist_control(Ctl* ctl, const double*
     double t1[5];
     for (int q = 0; q < 5; ++q) t1[q] = __ldcg(xsums + q);
     pdhg_control(ctl, t1, t3, token);
+    if (ctl->stop_mirror) reinterpret_cast<volatile int*>(ctl->stop_mirror)[token] = ctl->stop;
   }
 }
 

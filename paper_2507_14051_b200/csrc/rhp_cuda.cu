@@ -23,6 +23,7 @@
 #include <nccl.h>
 #endif
 
+#include "comm.cuh"
 #include "ingest.cuh"
 #include "layout.cuh"
 #include "op_kernels.cuh"
@@ -77,6 +78,36 @@ const NcclApi& nccl() {
     throw rhp::DeviceFailure("NCCL (libnccl.so.2) not found: the row-partitioned path needs it");
   return api;
 }
+
+// The production transport of comm.cuh: one NCCL communicator per rank.
+class NcclComm final : public rhp::Comm {
+ public:
+  NcclComm(const void* id128, int world, int rank) {
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    if (nccl().CommInitRank(&comm_, world, id, rank) != ncclSuccess)
+      throw CudaError("ncclCommInitRank failed");
+  }
+  ~NcclComm() override {
+    if (comm_) nccl().CommDestroy(comm_);
+  }
+  void allreduce(double* buf, size_t count, bool max, cudaStream_t s) override {
+    if (nccl().AllReduce(buf, buf, count, ncclDouble, max ? ncclMax : ncclSum, comm_, s) != ncclSuccess)
+      throw CudaError("ncclAllReduce failed");
+  }
+  void allreduce_max_i64(int64_t* buf, size_t count, cudaStream_t s) override {
+    if (nccl().AllReduce(buf, buf, count, ncclInt64, ncclMax, comm_, s) != ncclSuccess)
+      throw CudaError("ncclAllReduce(int64 max) failed");
+  }
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    if (nccl().AllGather(send, recv, bytes, ncclChar, comm_, s) != ncclSuccess)
+      throw CudaError("ncclAllGather failed");
+  }
+  bool is_nccl() const override { return true; }
+
+ private:
+  ncclComm_t comm_ = nullptr;
+};
 #endif
 
 template <class F>
@@ -189,9 +220,14 @@ struct rhp_ctx {
   // the A^T apply in rhp_scale (a matrix whose CSC values were produced by an
   // earlier scaling differs from its CSR values in the last ulp)
   double* csc_src = nullptr;
-#ifdef RHP_WITH_NCCL
-  ncclComm_t comm = nullptr;
-#endif
+  // collectives of the partitioned path (comm.cuh): NCCL or an in-process group
+  std::unique_ptr<Comm> comm;
+  // plain-mode partitioned blocks: per-iteration stop flags written by
+  // k_dist_control into mapped pinned memory, polled a few iterations behind
+  // the launches so no collective is issued far past an on-device stop
+  int* stop_mirror = nullptr;       // host pointer [block_limit]
+  int* stop_mirror_dev = nullptr;   // its device alias
+  std::vector<cudaEvent_t> it_events;
 };
 
 namespace {
@@ -535,8 +571,8 @@ void setup_peers(rhp_ctx& c) {
   char* d_h = nullptr;
   CK(cudaMalloc(&d_h, sizeof(mine) * (c.world + 1)));
   CK(cudaMemcpy(d_h, &mine, sizeof(mine), cudaMemcpyHostToDevice));
-  if (nccl().AllGather(d_h, d_h + sizeof(mine), sizeof(mine), ncclChar, c.comm, c.stream) != ncclSuccess)
-    throw CudaError("ncclAllGather of the IPC handles failed");
+  if (!c.comm->is_nccl()) throw CudaError("the peer-memory exchange needs the NCCL transport");
+  c.comm->allgather(d_h, d_h + sizeof(mine), sizeof(mine), c.stream);
   std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(c.world));
   CK(cudaMemcpyAsync(all.data(), d_h + sizeof(mine), sizeof(mine) * c.world, cudaMemcpyDeviceToHost,
                      c.stream));
@@ -595,23 +631,11 @@ EpiAty epi_aty(rhp_ctx& c, int token) {
 }
 
 void allreduce(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
-#ifdef RHP_WITH_NCCL
-  if (nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, c.comm, s) != ncclSuccess)
-    throw CudaError("ncclAllReduce failed");
-#else
-  (void)c, (void)buf, (void)count, (void)s;
-  throw CudaError("built without NCCL");
-#endif
+  c.comm->allreduce(buf, count, false, s);
 }
 
 void allreduce_max(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
-#ifdef RHP_WITH_NCCL
-  if (nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, c.comm, s) != ncclSuccess)
-    throw CudaError("ncclAllReduce(max) failed");
-#else
-  (void)c, (void)buf, (void)count, (void)s;
-  throw CudaError("built without NCCL");
-#endif
+  c.comm->allreduce(buf, count, true, s);
 }
 
 void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false) {
@@ -930,6 +954,18 @@ int rhp_get_device_info(int device, rhp_device_info* info) {
   });
 }
 
+int rhp_local_group_create(int world, void** out) {
+  return guarded([&] {
+    if (world < 1) throw std::invalid_argument("rhp_local_group_create: world must be >= 1");
+    *out = new LocalGroup(world);
+  });
+}
+
+int rhp_local_group_destroy(void* group) {
+  delete static_cast<LocalGroup*>(group);
+  return RHPDHG_OK;
+}
+
 int rhp_nccl_unique_id(void* out128) {
   return guarded([&] {
 #ifdef RHP_WITH_NCCL
@@ -968,10 +1004,14 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     if (opt.block_limit < 1) opt.block_limit = 64;
     if (opt.world_size < 1 || opt.rank < 0 || opt.rank >= opt.world_size)
       throw std::invalid_argument("rhp_create: bad rank/world_size");
-    if (opt.world_size > 1 && !opt.nccl_id)
-      throw std::invalid_argument("rhp_create: world_size > 1 needs an NCCL unique id");
+    if (opt.world_size > 1 && !opt.nccl_id && !opt.local_group)
+      throw std::invalid_argument("rhp_create: world_size > 1 needs an NCCL unique id or a local group");
+    if (opt.nccl_id && opt.local_group)
+      throw std::invalid_argument("rhp_create: give an NCCL id or a local group, not both");
+    if (opt.local_group && static_cast<const LocalGroup*>(opt.local_group)->world != opt.world_size)
+      throw std::invalid_argument("rhp_create: local group size differs from world_size");
     // row-partitioned path (also with one rank when an id is given: parity tests)
-    c->dist = opt.nccl_id != nullptr;
+    c->dist = opt.nccl_id != nullptr || opt.local_group != nullptr;
     c->rank = opt.rank;
     c->world = opt.world_size;
     if (c->dist) opt.use_graph = 0;  // NCCL calls are launched from the host loop
@@ -1081,15 +1121,23 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       c->ypad = dev_alloc<double>(static_cast<size_t>(c->max_local));
       c->ygather = dev_alloc<double>(static_cast<size_t>(c->max_local) * c->world);
       c->agree = dev_alloc<int64_t>(1);
+      if (opt.local_group) {
+        c->comm = std::make_unique<LocalComm>(
+            static_cast<LocalGroup*>(const_cast<void*>(opt.local_group)), c->rank);
+      } else {
 #ifdef RHP_WITH_NCCL
-      ncclUniqueId id;
-      std::memcpy(&id, opt.nccl_id, sizeof(id));
-      if (nccl().CommInitRank(&c->comm, c->world, id, c->rank) != ncclSuccess)
-        throw CudaError("ncclCommInitRank failed");
-      if (const char* e = std::getenv("RHP_PEER_EXCHANGE"); e && e[0] == '1') setup_peers(*c);
+        c->comm = std::make_unique<NcclComm>(opt.nccl_id, c->world, c->rank);
 #else
-      throw CudaError("built without NCCL");
+        throw CudaError("built without NCCL");
 #endif
+      }
+      if (const char* e = std::getenv("RHP_PEER_EXCHANGE"); e && e[0] == '1') setup_peers(*c);
+      CK(cudaHostAlloc(&c->stop_mirror, sizeof(int) * static_cast<size_t>(opt.block_limit),
+                       cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->stop_mirror_dev), c->stop_mirror, 0));
+      c->it_events.resize(static_cast<size_t>(opt.block_limit));
+      for (cudaEvent_t& e : c->it_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      SET_CTL(*c, stop_mirror, c->stop_mirror_dev);
     }
   });
   if (rc != RHPDHG_OK) {
@@ -1119,9 +1167,9 @@ int rhp_destroy(rhp_ctx* c) {
   if (c->csc_src) cudaFree(c->csc_src);
   if (c->res_a_split) cudaFree(c->res_a_split);
   if (c->res_at_split) cudaFree(c->res_at_split);
-#ifdef RHP_WITH_NCCL
-  if (c->comm) nccl().CommDestroy(c->comm);
-#endif
+  c->comm.reset();
+  if (c->stop_mirror) cudaFreeHost(c->stop_mirror);
+  for (cudaEvent_t e : c->it_events) cudaEventDestroy(e);
   if (c->ctl) cudaFree(c->ctl);
   if (c->ctl_host) cudaFreeHost(c->ctl_host);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1386,7 +1434,25 @@ int rhp_run_block(rhp_ctx* c, rhp_block_out* out) {
       if (c->host_iteration_limit != INT64_MAX)
         L = std::min<int64_t>(L, std::max<int64_t>(1, c->host_iteration_limit - c->host_total));
       launch_primal_init(*c, s);
-      for (int64_t i = 0; i < L; ++i) launch_iteration(*c, static_cast<int>(i), s);
+      if (!c->dist) {
+        for (int64_t i = 0; i < L; ++i) launch_iteration(*c, static_cast<int>(i), s);
+      } else {
+        // partitioned: iteration i's control kernel writes its stop flag to
+        // mapped host memory; the host launches at most kPollAhead iterations
+        // past the last flag it has seen, so after an on-device stop (restart
+        // verdict mid-block) at most kPollAhead no-op iterations, and their
+        // collectives, are issued — instead of the rest of the block
+        constexpr int64_t kPollAhead = 2;
+        std::fill(c->stop_mirror, c->stop_mirror + L, 0);
+        for (int64_t i = 0; i < L; ++i) {
+          if (i >= kPollAhead) {
+            CK(cudaEventSynchronize(c->it_events[i - kPollAhead]));
+            if (reinterpret_cast<volatile int*>(c->stop_mirror)[i - kPollAhead]) break;
+          }
+          launch_iteration(*c, static_cast<int>(i), s);
+          CK(cudaEventRecord(c->it_events[i], s));
+        }
+      }
     }
     CK(cudaEventRecord(c->ev1, s));
     pull_ctl(*c);
@@ -1440,13 +1506,11 @@ int rhp_kkt_of(rhp_ctx* c, const double* x, const double* y, rhp_kkt_sums* out) 
 // Row-partitioned: every rank receives the full m-vector (rank blocks are
 // contiguous original rows; NCCL allgather of the padded local blocks).
 void gather_rows(rhp_ctx& c, const double* dev_local, double* host_full) {
-#ifdef RHP_WITH_NCCL
   cudaStream_t s = c.stream;
   const size_t ml = static_cast<size_t>(c.m), mx = static_cast<size_t>(c.max_local);
   CK(cudaMemsetAsync(c.ypad, 0, std::max<size_t>(mx, 1) * sizeof(double), s));
   if (ml) CK(cudaMemcpyAsync(c.ypad, dev_local, ml * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (nccl().AllGather(c.ypad, c.ygather, mx, ncclDouble, c.comm, s) != ncclSuccess)
-    throw CudaError("ncclAllGather failed");
+  c.comm->allgather(c.ypad, c.ygather, mx * sizeof(double), s);
   std::vector<double> all(mx * static_cast<size_t>(c.world));
   if (!all.empty())
     CK(cudaMemcpyAsync(all.data(), c.ygather, all.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1456,10 +1520,6 @@ void gather_rows(rhp_ctx& c, const double* dev_local, double* host_full) {
     std::copy(all.begin() + static_cast<ptrdiff_t>(r * mx),
               all.begin() + static_cast<ptrdiff_t>(r * mx + (c.offsets[r + 1] - c.offsets[r])),
               host_full + c.offsets[r]);
-#else
-  (void)c, (void)dev_local, (void)host_full;
-  throw CudaError("built without NCCL");
-#endif
 }
 
 int rhp_fetch_solution(rhp_ctx* c, double* x, double* y, double* rcost) {
@@ -1487,15 +1547,12 @@ int rhp_any(rhp_ctx* c, int flag, int* any) {
       *any = flag;
       return;
     }
-#ifdef RHP_WITH_NCCL
     int64_t v = flag ? 1 : 0;
     CK(cudaMemcpyAsync(c->agree, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
-    if (nccl().AllReduce(c->agree, c->agree, 1, ncclInt64, ncclMax, c->comm, c->stream) != ncclSuccess)
-      throw CudaError("ncclAllReduce(agree) failed");
+    c->comm->allreduce_max_i64(c->agree, 1, c->stream);
     CK(cudaMemcpyAsync(&v, c->agree, sizeof v, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     *any = v != 0;
-#endif
   });
 }
 

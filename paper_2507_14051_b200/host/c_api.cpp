@@ -197,6 +197,19 @@ int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id) {
     } else {
       d.nccl_id.clear();
     }
+    d.local_group = nullptr;
+  });
+}
+
+int rhpdhg_set_local_group(int rank, int world_size, const void* group) {
+  return guarded([&] {
+    if (world_size < 1 || rank < 0 || rank >= world_size) throw UsageError("bad rank/world_size");
+    if (!group) throw UsageError("rhpdhg_set_local_group: null group");
+    DeviceOptions& d = default_device_options();
+    d.rank = rank;
+    d.world_size = world_size;
+    d.nccl_id.clear();
+    d.local_group = group;
   });
 }
 

@@ -69,6 +69,7 @@ inline rhp_options options(int device, bool use_graph, long block_limit) {
   o.use_graph = use_graph ? 1 : 0;
   o.block_limit = block_limit;
   o.nccl_id = nullptr;
+  o.local_group = nullptr;
   o.resident = 0;  // per-op contexts (products, KKT, scaling) never use resident blocks
   return o;
 }
@@ -84,8 +85,10 @@ inline rhp_options options(const DeviceOptionsT& d) {
   if (!d.nccl_id.empty()) {
     if (d.nccl_id.size() != 128) throw UsageError("nccl_id must be 128 bytes");
     o.nccl_id = d.nccl_id.data();
+  } else if (d.local_group) {
+    o.local_group = d.local_group;
   } else if (d.world_size > 1) {
-    throw UsageError("world_size > 1 needs the NCCL unique id of rank 0");
+    throw UsageError("world_size > 1 needs the NCCL unique id of rank 0 or a local group");
   }
   return o;
 }

@@ -13,11 +13,26 @@
 //     warning); integrality markers and integer bounds are relaxed with a
 //     warning;
 //   * maximisation negates the objective and offset (LpProblem convention).
+//
+// Parallel fast path: the text is split into lines
+// by all host threads; NAME / OBJSENSE / ROWS and the sections after COLUMNS
+// run through the sequential Reader line by line, while the COLUMNS body —
+// nearly all of a large file — is tokenized, its row names resolved and its
+// numbers parsed by one thread per line chunk; a sequential merge assigns
+// column indices in order of first appearance and the matrix is assembled
+// directly as CSR (no triplet sort). Anything unusual in the parallel part
+// (a malformed line, an unknown row, a non-finite or duplicate entry) makes
+// the reader re-parse the whole text with the sequential Reader, so errors,
+// their line numbers and warnings are exactly the sequential reader's.
 #include <zlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cctype>
+#include <charconv>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <fstream>
 #include <functional>
 #include <limits>
@@ -25,6 +40,8 @@
 #include <set>
 #include <sstream>
 #include <string>
+#include <string_view>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -62,6 +79,14 @@ double number(const std::string& text, long line) {
   return v;
 }
 
+// string-keyed maps that also accept string_view lookups (no allocation)
+struct NameHash {
+  using is_transparent = void;
+  size_t operator()(std::string_view v) const { return std::hash<std::string_view>{}(v); }
+};
+template <class V>
+using NameMap = std::unordered_map<std::string, V, NameHash, std::equal_to<>>;
+
 struct Row {
   char sense = 'N';
   Index index = -1;  // constraint index, -1 for N rows
@@ -84,21 +109,65 @@ class Reader {
   LpProblem read(std::istream& in) {
     std::string text;
     while (std::getline(in, text)) {
-      ++line_;
-      if (!text.empty() && text.back() == '\r') text.pop_back();
-      if (text.empty() || text[0] == '*') continue;
-      const std::vector<std::string> f = tokens(text);
-      if (!std::isspace(static_cast<unsigned char>(text[0]))) {
-        header(f);
-        if (part_ == Part::endata) break;
-        continue;
-      }
-      if (f.empty()) continue;
-      body(f);
+      if (!line(text, line_ + 1)) break;
     }
+    return end();
+  }
+
+  // One input line (1-based number `no`); false once ENDATA was read.
+  bool line(std::string_view text, long no) {
+    line_ = no;
+    if (!text.empty() && text.back() == '\r') text.remove_suffix(1);
+    if (text.empty() || text[0] == '*') return true;
+    const std::vector<std::string> f = tokens(std::string(text));
+    if (!std::isspace(static_cast<unsigned char>(text[0]))) {
+      header(f);
+      return part_ != Part::endata;
+    }
+    if (f.empty()) return true;
+    body(f);
+    return true;
+  }
+
+  LpProblem end() {
     if (part_ != Part::endata) throw ParseError("missing ENDATA", line_);
     return finish();
   }
+
+  Part part() const { return part_; }
+
+  // ---- hooks of the parallel COLUMNS path (ParallelReader) ----
+  const NameMap<Row>& rows() const { return rows_; }
+  // Column index of `name` (assigned in order of first appearance).
+  Index column_index(std::string_view name) {
+    auto it = cols_.find(name);
+    if (it == cols_.end()) {
+      it = cols_.emplace(std::string(name), Col{}).first;
+      it->second.index = n_++;
+      c_.push_back(0.0);
+      obj_flag_.push_back(0);
+    }
+    return it->second.index;
+  }
+  // Objective coefficient of column j; false on a duplicate (sequential
+  // reader reports it).
+  bool objective_entry(Index j, double v) {
+    if (obj_flag_[static_cast<size_t>(j)]) return false;
+    obj_flag_[static_cast<size_t>(j)] = 1;
+    c_[static_cast<size_t>(j)] = v;
+    return true;
+  }
+  void note_at(long no, const std::string& msg) {
+    if (warnings_) warnings_->push_back("line " + std::to_string(no) + ": " + msg);
+    int_noted_ = true;
+  }
+  bool int_noted() const { return int_noted_; }
+  void set_matrix(SparseMatrix a) {
+    matrix_ = std::move(a);
+    have_matrix_ = true;
+  }
+  Index num_rows() const { return m_; }
+  Index num_cols() const { return n_; }
 
  private:
   void note(const std::string& msg) {
@@ -192,6 +261,7 @@ class Reader {
     if (fresh) {
       it->second.index = n_++;
       c_.push_back(0.0);
+      obj_flag_.push_back(0);
     }
     const Index j = it->second.index;
     for (size_t k = 1; k + 1 < f.size(); k += 2) {
@@ -274,7 +344,7 @@ class Reader {
     if (objective_.empty()) throw ParseError("no objective (N) row declared", 0);
     LpProblem p;
     p.name = name_;
-    p.matrix = SparseMatrix(m_, n_, std::move(triplets_));
+    p.matrix = have_matrix_ ? std::move(matrix_) : SparseMatrix(m_, n_, std::move(triplets_));
     p.objective = std::move(c_);
     p.objective_offset = offset_;
     p.con_lb.assign(static_cast<size_t>(m_), 0.0);
@@ -313,36 +383,273 @@ class Reader {
   bool maximize_ = false, int_noted_ = false;
   double offset_ = 0.0;
   Index m_ = 0, n_ = 0;
-  std::unordered_map<std::string, Row> rows_;
-  std::unordered_map<std::string, Col> cols_;
+  NameMap<Row> rows_;
+  NameMap<Col> cols_;
   std::vector<double> c_;
   std::set<std::pair<Index, Index>> seen_;
   std::set<Index> obj_seen_;
   std::vector<Triplet> triplets_;
+  std::vector<char> obj_flag_;
+  SparseMatrix matrix_;
+  bool have_matrix_ = false;
 };
+
+// ------------------------------------------------------- parallel reader --
+// Signals that the fast path met something only the sequential reader
+// handles exactly (it then re-parses the text).
+struct Fallback {};
+
+unsigned worker_count() {
+  const unsigned t = std::thread::hardware_concurrency();
+  return std::max(1u, std::min(t ? t : 1u, 64u));
+}
+
+template <class F>
+void parallel_for(size_t parts, const F& f) {
+  std::vector<std::thread> pool;
+  for (size_t p = 1; p < parts; ++p) pool.emplace_back(f, p);
+  f(0);
+  for (std::thread& t : pool) t.join();
+}
+
+// Byte offsets of every line start (plus the end), by all threads.
+std::vector<size_t> line_starts(std::string_view text) {
+  const size_t T = text.size() < (1u << 20) ? 1 : worker_count();
+  std::vector<std::vector<size_t>> part(T);
+  parallel_for(T, [&](size_t t) {
+    const size_t b = text.size() * t / T, e = text.size() * (t + 1) / T;
+    const char* p = text.data();
+    for (size_t i = b; i < e; ++i)
+      if (p[i] == '\n') part[t].push_back(i + 1);
+  });
+  std::vector<size_t> out{0};
+  size_t total = 1;
+  for (auto& v : part) total += v.size();
+  out.reserve(total + 1);
+  for (auto& v : part) out.insert(out.end(), v.begin(), v.end());
+  if (out.back() != text.size()) out.push_back(text.size());
+  return out;
+}
+
+bool is_space(char ch) { return ch == ' ' || ch == '\t' || ch == '\r' || ch == '\v' || ch == '\f' || ch == '\n'; }
+
+// Whitespace fields of a line as views; at most `cap` (more -> n = cap + 1).
+size_t fields(std::string_view line, std::string_view* out, size_t cap) {
+  size_t n = 0, i = 0;
+  while (i < line.size()) {
+    while (i < line.size() && is_space(line[i])) ++i;
+    if (i >= line.size()) break;
+    const size_t b = i;
+    while (i < line.size() && !is_space(line[i])) ++i;
+    if (n < cap) out[n] = line.substr(b, i - b);
+    ++n;
+  }
+  return n;
+}
+
+// number() of the sequential reader without allocation on the common path
+// (Fortran 'D' exponents and forms from_chars rejects take the exact path).
+bool fast_number(std::string_view t, double& v) {
+  const char* b = t.data();
+  const char* e = b + t.size();
+  if (t.empty() || *b == '+' || t.find_first_of("Dd") != std::string_view::npos) return false;
+  const auto r = std::from_chars(b, e, v);
+  return r.ec == std::errc() && r.ptr == e && std::isfinite(v);
+}
+
+struct ColEntry {
+  Index row;   // constraint index; -1 objective; -2 another N row (ignored)
+  double value;
+};
+struct ColLine {
+  std::string_view column;
+  uint32_t first, count;  // entries [first, first + count) of the chunk
+  long no;                // line number (for the integrality note)
+  bool intorg;            // an INTORG marker line
+};
+
+LpProblem parse_text(std::string_view text, std::vector<std::string>* warnings) {
+  std::vector<std::string> warn;
+  Reader rd(&warn);
+  const std::vector<size_t> ls = line_starts(text);
+  const size_t L = ls.size() - 1;
+  auto line_at = [&](size_t i) {
+    std::string_view v = text.substr(ls[i], ls[i + 1] - ls[i]);
+    if (!v.empty() && v.back() == '\n') v.remove_suffix(1);
+    return v;
+  };
+  bool ended = false;
+  size_t i = 0;
+  while (i < L && !ended) {
+    if (rd.part() == Part::columns) {
+      // the COLUMNS body: lines up to the next header, in parallel
+      size_t j = i;
+      for (; j < L; ++j) {
+        const std::string_view v = line_at(j);
+        if (!v.empty() && v[0] != '*' && v[0] != '\r' && !is_space(v[0])) break;
+      }
+      const size_t T = (j - i) < 4096 ? 1 : worker_count();
+      std::vector<std::vector<ColLine>> lines(T);
+      std::vector<std::vector<ColEntry>> ents(T);
+      std::atomic<bool> bad{false};
+      const NameMap<Row>& rows = rd.rows();
+      parallel_for(T, [&](size_t t) {
+        const size_t b = i + (j - i) * t / T, e = i + (j - i) * (t + 1) / T;
+        std::string_view f[64];
+        for (size_t k = b; k < e && !bad.load(std::memory_order_relaxed); ++k) {
+          std::string_view v = line_at(k);
+          if (!v.empty() && v.back() == '\r') v.remove_suffix(1);
+          if (v.empty() || v[0] == '*') continue;
+          const size_t nf = fields(v, f, 64);
+          if (nf == 0) continue;
+          if (nf > 64) { bad = true; break; }
+          bool marker = false, intorg = false;
+          for (size_t q = 0; q < nf; ++q) {
+            marker |= f[q] == "'MARKER'" || f[q] == "\"MARKER\"";
+            intorg |= f[q] == "'INTORG'" || f[q] == "\"INTORG\"";
+          }
+          if (marker) {
+            lines[t].push_back({std::string_view(), 0, 0, static_cast<long>(k + 1), intorg});
+            continue;
+          }
+          if (nf < 3 || nf % 2 == 0) { bad = true; break; }
+          ColLine cl{f[0], static_cast<uint32_t>(ents[t].size()), 0, static_cast<long>(k + 1), false};
+          for (size_t q = 1; q + 1 < nf; q += 2) {
+            const auto it = rows.find(f[q]);
+            double val;
+            if (it == rows.end() || !fast_number(f[q + 1], val)) { bad = true; break; }
+            const Row& r = it->second;
+            ents[t].push_back({r.sense == 'N' ? (r.objective ? -1 : -2) : r.index, val});
+          }
+          if (bad) break;
+          cl.count = static_cast<uint32_t>(ents[t].size() - cl.first);
+          lines[t].push_back(cl);
+        }
+      });
+      if (bad) throw Fallback{};
+      // sequential merge: column indices, objective, per-row counts
+      const Index m = rd.num_rows();
+      std::vector<Index> rp(static_cast<size_t>(m) + 1, 0);
+      std::vector<std::vector<Index>> jcol(T);
+      std::string_view prev;
+      Index pj = -1;
+      for (size_t t = 0; t < T; ++t) {
+        jcol[t].resize(ents[t].size());
+        for (const ColLine& cl : lines[t]) {
+          if (cl.column.empty()) {  // marker line
+            if (cl.intorg && !rd.int_noted())
+              rd.note_at(cl.no, "integrality markers ignored; variables relaxed to their continuous box");
+            continue;
+          }
+          if (pj < 0 || cl.column != prev) {
+            pj = rd.column_index(cl.column);
+            prev = cl.column;
+          }
+          for (uint32_t q = cl.first; q < cl.first + cl.count; ++q) {
+            const ColEntry& en = ents[t][q];
+            jcol[t][q] = pj;
+            if (en.row == -1) {
+              if (!rd.objective_entry(pj, en.value)) throw Fallback{};
+            } else if (en.row >= 0) {
+              ++rp[static_cast<size_t>(en.row) + 1];
+            }
+          }
+        }
+      }
+      for (Index r = 0; r < m; ++r) rp[r + 1] += rp[r];
+      // CSR in line order (stable per row), zeros dropped by from_csr
+      std::vector<Index> ci(static_cast<size_t>(rp[m]));
+      std::vector<double> cv(static_cast<size_t>(rp[m]));
+      std::vector<Index> fill(rp.begin(), rp.end() - 1);
+      for (size_t t = 0; t < T; ++t)
+        for (size_t q = 0; q < ents[t].size(); ++q) {
+          const ColEntry& en = ents[t][q];
+          if (en.row < 0) continue;
+          const Index s2 = fill[static_cast<size_t>(en.row)]++;
+          ci[static_cast<size_t>(s2)] = jcol[t][q];
+          cv[static_cast<size_t>(s2)] = en.value;
+        }
+      // a column that reappears later breaks the ascending order: sort such
+      // rows; a repeated (row, column) pair -> the sequential reader's error
+      for (Index r = 0; r < m; ++r) {
+        const size_t b = static_cast<size_t>(rp[r]), e = static_cast<size_t>(rp[r + 1]);
+        bool sorted = true;
+        for (size_t q = b + 1; q < e; ++q) sorted &= ci[q] > ci[q - 1];
+        if (sorted) continue;
+        std::vector<std::pair<Index, double>> row;
+        for (size_t q = b; q < e; ++q) row.emplace_back(ci[q], cv[q]);
+        std::stable_sort(row.begin(), row.end(),
+                         [](const auto& a, const auto& c) { return a.first < c.first; });
+        for (size_t q = 1; q < row.size(); ++q)
+          if (row[q].first == row[q - 1].first) throw Fallback{};
+        for (size_t q = b; q < e; ++q) {
+          ci[q] = row[q - b].first;
+          cv[q] = row[q - b].second;
+        }
+      }
+      rd.set_matrix(SparseMatrix::from_csr(m, rd.num_cols(), std::move(rp), std::move(ci), std::move(cv)));
+      // the header that ends COLUMNS (the section cannot be re-entered)
+      if (j < L) ended = !rd.line(line_at(j), static_cast<long>(j + 1));
+      i = j + 1;
+      continue;
+    }
+    ended = !rd.line(line_at(i), static_cast<long>(i + 1));
+    ++i;
+  }
+  if (!ended) rd.line(std::string_view(), static_cast<long>(L));  // line_ for "missing ENDATA"
+  LpProblem p = rd.end();
+  if (warnings) warnings->insert(warnings->end(), warn.begin(), warn.end());
+  return p;
+}
+
+}  // namespace
+
+namespace {
+
+// The whole text: the parallel reader, or on any irregularity the sequential
+// reader (exact errors, line numbers and warnings).
+LpProblem parse_all(const std::string& data, std::vector<std::string>* warnings) {
+  const char* seq = std::getenv("RHPDHG_MPS_SEQUENTIAL");  // 1: the sequential reader only
+  if (!(seq && seq[0] == '1')) try {
+    return parse_text(data, warnings);
+  } catch (const Fallback&) {
+  } catch (const ParseError&) {
+  } catch (const InvalidProblemError&) {
+  } catch (const UsageError&) {
+  }
+  std::istringstream in(data);
+  return Reader(warnings).read(in);
+}
 
 }  // namespace
 
 LpProblem parse_mps(std::istream& in, std::vector<std::string>* warnings) {
-  return Reader(warnings).read(in);
+  std::string data((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  return parse_all(data, warnings);
 }
 
 LpProblem parse_mps_file(const std::string& path, std::vector<std::string>* warnings) {
+  std::string data;
   if (path.size() > 3 && path.compare(path.size() - 3, 3, ".gz") == 0) {
     gzFile gz = gzopen(path.c_str(), "rb");
     if (!gz) throw ParseError("cannot open '" + path + "'", 0);
-    std::string data;
-    char buf[1 << 16];
+    gzbuffer(gz, 1 << 20);
+    std::vector<char> buf(1 << 22);
     int k = 0;
-    while ((k = gzread(gz, buf, sizeof buf)) > 0) data.append(buf, static_cast<size_t>(k));
+    while ((k = gzread(gz, buf.data(), static_cast<unsigned>(buf.size()))) > 0)
+      data.append(buf.data(), static_cast<size_t>(k));
     gzclose(gz);
     if (k < 0) throw ParseError("gzip read error in '" + path + "'", 0);
-    std::istringstream in(data);
-    return parse_mps(in, warnings);
+  } else {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw ParseError("cannot open '" + path + "'", 0);
+    in.seekg(0, std::ios::end);
+    const std::streamoff size = in.tellg();
+    in.seekg(0, std::ios::beg);
+    data.resize(static_cast<size_t>(std::max<std::streamoff>(size, 0)));
+    if (size > 0) in.read(data.data(), size);
   }
-  std::ifstream in(path);
-  if (!in) throw ParseError("cannot open '" + path + "'", 0);
-  return parse_mps(in, warnings);
+  return parse_all(data, warnings);
 }
 
 }  // namespace rhpdhg

@@ -108,7 +108,7 @@ void log_progress(const SolverConfig& cfg, long iter, double fpr, const KktResid
 }  // namespace
 
 DeviceOptions& default_device_options() {
-  static DeviceOptions opts;
+  thread_local DeviceOptions opts;
   return opts;
 }
 

@@ -395,6 +395,34 @@ def set_distributed(rank: int = 0, world_size: int = 1, nccl_id: bytes | None = 
                  lib.rhpdhg_last_error().decode(errors="replace"))
 
 
+class LocalGroup:
+    """In-process collective group (rhp_local_group_create): `world` threads
+    of this process, each calling set_local_group(rank, world, group) and
+    then solving the same LP, run the row-partitioned engine together; their
+    exchanges go through device memory with rank-ordered reductions."""
+
+    def __init__(self, world: int):
+        self._lib = capi.load_cuda()
+        h = C.c_void_p()
+        raise_status(self._lib.rhp_local_group_create(world, C.byref(h)),
+                     self._lib.rhp_last_error().decode(errors="replace"))
+        self.handle = h
+        self.world = world
+
+    def close(self):
+        if self.handle:
+            self._lib.rhp_local_group_destroy(self.handle)
+            self.handle = None
+
+
+def set_local_group(rank: int, world_size: int, group: "LocalGroup") -> None:
+    """This THREAD acts as `rank` of an in-process group (device options are
+    per thread)."""
+    lib = capi.load_host()
+    raise_status(lib.rhpdhg_set_local_group(rank, world_size, group.handle),
+                 lib.rhpdhg_last_error().decode(errors="replace"))
+
+
 def partition_rows(lp: LpProblem, world_size: int) -> np.ndarray:
     """The row partition the multi-GPU path uses (GPU-free host logic)."""
     lib = capi.load_cuda()

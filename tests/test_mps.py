@@ -104,3 +104,61 @@ def test_loader_matches_reference_parser_on_its_fixtures():
             continue
         got, _ = read_mps(f)
         same_lp(got, want)
+
+
+# ---------------------------------------------------------------- parallel --
+def _mps_variants(tmp_path):
+    """Texts that exercise the parallel COLUMNS path and its fallbacks."""
+    from paper_2507_14051_b200.generators import c1_small, random_rows_lp
+
+    out = []
+    big = random_rows_lp(3, 3000, 5000, np.full(3000, 40))
+    p = tmp_path / "big.mps"
+    write_mps(big, p)
+    out.append(p)
+    with open(p, "rb") as f, gzip.open(str(tmp_path / "big.mps.gz"), "wb") as g:
+        g.write(f.read())
+    out.append(tmp_path / "big.mps.gz")
+    # a column that reappears after others (rows must be re-sorted), markers,
+    # CRLF line ends and comment lines inside COLUMNS
+    lp = c1_small(m=300, n=400)
+    p2 = tmp_path / "c1.mps"
+    write_mps(lp, p2)
+    lines = p2.read_text().splitlines()
+    ci = lines.index("COLUMNS")
+    body = lines[ci + 1:lines.index("RHS")]
+    moved = [l for l in body if l.split()[0] == "X7" and "OBJ" not in l]
+    keep = [l for l in body if l not in moved]
+    new = (lines[:ci + 1] + ["    MARKER 'MARKER' 'INTORG'"] + keep[:50] +
+           ["* a comment", "    MARKER 'MARKER' 'INTEND'"] + keep[50:] + moved +
+           lines[lines.index("RHS"):])
+    p3 = tmp_path / "reordered.mps"
+    p3.write_bytes(("\r\n".join(new) + "\r\n").encode())
+    out.append(p3)
+    # a duplicate entry (fallback: the sequential reader's ParseError)
+    dup = lines[:ci + 1] + body + [body[-1]] + lines[lines.index("RHS"):]
+    p4 = tmp_path / "dup.mps"
+    p4.write_text("\n".join(dup) + "\n")
+    out.append(p4)
+    return out
+
+
+def test_parallel_reader_equals_sequential_reader(tmp_path, monkeypatch):
+    for path in _mps_variants(tmp_path):
+        monkeypatch.delenv("RHPDHG_MPS_SEQUENTIAL", raising=False)
+        try:
+            got, gw = read_mps(path)
+            gerr = None
+        except ParseError as e:
+            got, gerr = None, str(e)
+        monkeypatch.setenv("RHPDHG_MPS_SEQUENTIAL", "1")
+        try:
+            want, ww = read_mps(path)
+            werr = None
+        except ParseError as e:
+            want, werr = None, str(e)
+        assert gerr == werr, path
+        if want is not None:
+            same_lp(got, want)
+            assert gw == ww, path
+    assert werr is not None and "duplicate entry" in werr  # the last variant

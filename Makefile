@@ -8,7 +8,7 @@ LIB      := $(PKG)/lib
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v \
             --expt-relaxed-constexpr -DRHP_WITH_NCCL
-CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/host
+CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/host -isystem /usr/local/cuda/include
 
 CU_SRCS  := $(PKG)/csrc/rhp_cuda.cu $(PKG)/csrc/layout.cu $(PKG)/csrc/ingest.cu $(PKG)/csrc/segments.cu $(PKG)/csrc/ops.cu
 CU_HDRS  := $(wildcard $(PKG)/csrc/*.cuh) include/rhpdhg_cuda.h include/rhpdhg_c.h
@@ -23,7 +23,7 @@ $(LIB)/librhp_cuda.so: $(CU_SRCS) $(CU_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) -ldl 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
 $(LIB)/librhpdhg.so: $(HOST_SRCS) $(HOST_HDRS) $(LIB)/librhp_cuda.so
-	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -lrhp_cuda -lz -Wl,-rpath,'$$ORIGIN'
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIB) -lrhp_cuda -lz -ldl -pthread -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle oracle

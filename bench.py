@@ -500,17 +500,17 @@ def run_product(args):
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
         if args.config == "c5":
             small = generators.c5_rowpart(**C5_CPU_SAMPLE)
-            cpu = cpu_sample(small, args.cpu_iters, "C5 generator at 1/50 scale", "c2")
+            cpu = cpu_sample(small, args.cpu_iters or 64, "C5 generator at 1/50 scale", "c2")
             ratio = lp.nnz / small.nnz
             cpu["value"] /= ratio
             cpu["setup_seconds"] *= ratio
             cpu["sample"] = (f"the reference on the C5 generator at m={small.num_cons}, "
-                             f"n={small.num_vars}, {small.nnz} nnz (setup + {args.cpu_iters} "
+                             f"n={small.num_vars}, {small.nnz} nnz (setup + {args.cpu_iters or 64} "
                              f"iterations, 1 thread); iter/s and setup extrapolated linearly in "
                              f"nonzeros (x{ratio:.1f})")
         else:
-            iters = args.cpu_iters if args.cpu_iters else (8 if args.config in BOUNDED else 64)
-            cpu = cpu_sample(lp, iters, WORKLOADS[args.config], args.config)
+            n_cpu = args.cpu_iters if args.cpu_iters else (8 if args.config in BOUNDED else 64)
+            cpu = cpu_sample(lp, n_cpu, WORKLOADS[args.config], args.config)
         if e2e and e2e["status"] == "optimal":
             it = e2e["iterations"]
             cpu["time_to_tol_extrapolated_s"] = cpu["setup_seconds"] + it / cpu["value"]

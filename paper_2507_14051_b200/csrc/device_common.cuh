@@ -132,6 +132,10 @@ constexpr double kGatherL2Bytes = 32.0 * 1024 * 1024;
 // Operators whose longest row has at most kThreadRowMax nonzeros use the
 // thread-per-row engine (spmv.cuh thread_rows; rhp_cuda.cu choose_engines).
 constexpr int64_t kThreadRowMax = 8;
+// Operators whose every row has at least kCtaRowMin nonzeros use the long-row
+// engine (spmv.cuh spmv_cta_rows), kCtaRowsBatch rows per CTA pass.
+constexpr int64_t kCtaRowMin = 256;
+constexpr int kCtaRowsBatch = 8;
 #ifndef RHP_ROWS_IN_FLIGHT
 #define RHP_ROWS_IN_FLIGHT 2
 #endif

@@ -156,6 +156,8 @@ struct DevOp : DeviceCsr {
   // every schedule-dependent use goes through fin() (the last segment)
   std::vector<DevOp> segs;
   double* segbuf = nullptr;  // [rows] running row sums of the segments
+  // long-row engine (spmv_cta_rows): CTA b owns rows [cta_row[b], cta_row[b+1])
+  int32_t* cta_row = nullptr;
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
 
@@ -182,6 +184,15 @@ struct rhp_ctx {
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;  // pinned mirror
   int grid_a = 1, grid_at = 1, grid_vec = 1, grid_max = 1;
+  // Row-partitioned: the n-side walkers (block-start primal step, K2c, KKT
+  // column sums, power-iteration dots) use this rank-INDEPENDENT map — one
+  // column per thread, grid vec_grid(n) — instead of the local A_p^T
+  // schedule, whose chunks differ per rank: every rank then sums its x-side
+  // partials in the same order, so the residual, the restart verdict, the PID
+  // weight and ||A|| are bit-identical on all ranks (decisions cannot diverge
+  // and desynchronise the collectives).
+  Sched nside{};
+  int grid_nside = 1;
   // CUDA graph of one block of iterations
   bool graph_built = false;
   cudaGraph_t graph = nullptr;
@@ -278,7 +289,7 @@ void free_op(DevOp& d) {
   for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.warp_row,
                   (void*)d.warp_nz, (void*)d.slot_row, (void*)d.head_slot, (void*)d.tail_slot,
                   (void*)d.slot_first, (void*)d.slot_count, (void*)d.slot_part,
-                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.segbuf})
+                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.segbuf, (void*)d.cta_row})
     if (p) cudaFree(p);
   d = DevOp{};
 }
@@ -287,6 +298,13 @@ void free_op(DevOp& d) {
 // segment of a segmented operator, else the operator itself. K3 and the
 // partitioned walkers walk its schedule and K1's finalize reads its slots.
 const DevOp& fin(const DevOp& op) { return op.segs.empty() ? op : op.segs.back(); }
+
+// The map of the n-side walkers and of the x-side partials (part3 layout):
+// single GPU: A^T's schedule (K3 bit-identical to K2's fused primal step);
+// row-partitioned: the rank-independent column map (rhp_ctx::nside).
+const Sched& nside_sched(const rhp_ctx& c);
+int nside_grid(const rhp_ctx& c);
+const double* nside_long_red(const rhp_ctx& c);
 
 // First index of a contiguous ascending permutation (the layout keeps rows
 // and columns in their original order, so every map is one), else -1.
@@ -358,6 +376,12 @@ void launch_one(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const E
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = c.pdl ? 1 : 0;
+  if (op.cta_row) {
+    const int32_t* cr = op.cta_row;
+    if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, true>, op.csr(), xg, op.sched, cr, epi, part, ticket));
+    else CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, false>, op.csr(), xg, op.sched, cr, epi, part, ticket));
+    return;
+  }
   if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
   else CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
 }
@@ -447,9 +471,38 @@ void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
   }
 }
 
+// Long-row engine (spmv.cuh spmv_cta_rows) for an operator whose every row
+// has >= kCtaRowMin nonzeros (C3's A: 2000 rows of 1000): CTA row runs
+// balanced by nonzeros over the operator's grid. Only for A — A^T's
+// schedule is also walked by K3 / the partitioned walkers, which need the
+// merge-path or thread-per-row map. RHP_CTA_ROWS=0 disables it.
+void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp, int grid) {
+  const char* env = std::getenv("RHP_CTA_ROWS");
+  if (env && env[0] == '0') return;
+  const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
+  if (rows < 1 || rows > INT32_MAX) return;
+  for (int64_t r = 0; r < rows; ++r)
+    if (rp[r + 1] - rp[r] < kCtaRowMin) return;
+  std::vector<int32_t> cr(static_cast<size_t>(grid) + 1, static_cast<int32_t>(rows));
+  cr[0] = 0;
+  const double total = static_cast<double>(rp[rows]);
+  int64_t r = 0;
+  for (int b = 1; b < grid; ++b) {
+    const double goal = total * b / grid;
+    while (r < rows && static_cast<double>(rp[r]) < goal) ++r;
+    cr[b] = static_cast<int32_t>(r);
+  }
+  d.cta_row = dev_alloc<int32_t>(cr.size());
+  upload(d.cta_row, cr.data(), cr.size(), c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  d.sched.thread_rows = 0;
+  d.sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
+}
+
 void choose_engines(rhp_ctx& c) {
   apply_engine_rule(c.A, c.L.A.rp);
   apply_engine_rule(c.At, c.L.At.rp);
+  apply_cta_rule(c, c.A, c.L.A.rp, c.grid_a);
 }
 
 __global__ void k_mark_sectors(const int32_t* ci, int64_t lo, int64_t hi, unsigned int* bits) {
@@ -515,7 +568,7 @@ void build_segments(rhp_ctx& c, DevOp& d, const HostOperator& h, int64_t cols, i
   d.segbuf = nullptr;
   double seg_bytes = 64.0 * 1024 * 1024;  // C5: 48 MB 68, 64 MB 74.8, 80 MB 66.8 iter/s
   if (const char* e = std::getenv("RHP_SEG_BYTES")) seg_bytes = std::atof(e);
-  if (!(seg_bytes > 0) || d.nnz == 0) return;
+  if (!(seg_bytes > 0) || d.nnz == 0 || d.cta_row) return;
   const int64_t S = static_cast<int64_t>(std::ceil(static_cast<double>(cols) * 8.0 / seg_bytes));
   if (S <= 1) return;
   const char* force = std::getenv("RHP_SEG_FORCE");
@@ -603,6 +656,17 @@ void setup_peers(rhp_ctx& c) {
 #endif
 }
 
+// (one rank keeps A^T's schedule: nothing to agree with, and the one-rank
+// partitioned path stays bit-identical to the single-GPU path)
+bool rank_independent_nside(const rhp_ctx& c) { return c.dist && c.world > 1; }
+const Sched& nside_sched(const rhp_ctx& c) {
+  return rank_independent_nside(c) ? c.nside : fin(c.At).sched;
+}
+int nside_grid(const rhp_ctx& c) { return rank_independent_nside(c) ? c.grid_nside : c.grid_at; }
+const double* nside_long_red(const rhp_ctx& c) {
+  return rank_independent_nside(c) ? nullptr : fin(c.At).long_red;
+}
+
 EpiDual epi_dual(rhp_ctx& c, int token) {
   EpiDual e{};
   e.ctl = c.ctl;
@@ -612,9 +676,9 @@ EpiDual epi_dual(rhp_ctx& c, int token) {
   const double* in[] = {c.y, c.ax, c.cl, c.cu, c.y0, c.ax0};
   for (int k = 0; k < EpiDual::NIN; ++k) e.in[k] = in[k];
   e.part3 = c.part3;
-  e.grid3 = c.grid_at;
-  e.n_multi3 = fin(c.At).sched.n_multi;
-  e.long_red3 = fin(c.At).long_red;
+  e.grid3 = nside_grid(c);
+  e.n_multi3 = nside_sched(c).n_multi;
+  e.long_red3 = nside_long_red(c);
   e.token = token;
   return e;
 }
@@ -664,8 +728,8 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   } else {
     allreduce(c, c.xchg, static_cast<size_t>(c.n) + 5, s);
   }
-  k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, c.grid_at, fin(c.At).sched.n_multi,
-                                      fin(c.At).long_red, c.xchg + c.n, token);
+  k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, nside_grid(c), nside_sched(c).n_multi,
+                                      nside_long_red(c), c.xchg + c.n, token);
   CK(cudaGetLastError());
   EpiAtyDist e{};
   e.ctl = c.ctl;
@@ -674,7 +738,7 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   const double* in[] = {c.xchg, c.aty, c.aty0, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiAtyDist::NIN; ++k) e.in[k] = in[k];
   e.token = token;
-  epilogue_walk<EpiAtyDist><<<c.grid_at, kBlock, 0, s>>>(fin(c.At).sched, e, c.part3);
+  epilogue_walk<EpiAtyDist><<<nside_grid(c), kBlock, 0, s>>>(nside_sched(c), e, c.part3);
   CK(cudaGetLastError());
 }
 
@@ -789,7 +853,7 @@ void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
   e.o = primal_out(c);
   const double* in[] = {c.aty, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiPrimal::NIN; ++k) e.in[k] = in[k];
-  epilogue_walk<EpiPrimal><<<c.grid_at, kBlock, 0, s>>>(fin(c.At).sched, e, c.part3);
+  epilogue_walk<EpiPrimal><<<nside_grid(c), kBlock, 0, s>>>(nside_sched(c), e, c.part3);
   CK(cudaGetLastError());
 }
 
@@ -887,10 +951,10 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
     cd.col = ec;
     const double* in[] = {c.xchg, xs, c.cs, c.co, c.vlo, c.vuo};
     for (int k = 0; k < EpiKktColDist::NIN; ++k) cd.in[k] = in[k];
-    epilogue_walk<EpiKktColDist><<<c.grid_at, kBlock, 0, c.stream>>>(fin(c.At).sched, cd, c.partAt);
+    epilogue_walk<EpiKktColDist><<<nside_grid(c), kBlock, 0, c.stream>>>(nside_sched(c), cd, c.partAt);
     CK(cudaGetLastError());
-    k_kkt_dist_finalize<<<1, kBlock, 0, c.stream>>>(c.ctl, c.partAt, c.grid_at,
-                                                    fin(c.At).sched.n_multi, fin(c.At).long_red,
+    k_kkt_dist_finalize<<<1, kBlock, 0, c.stream>>>(c.ctl, c.partAt, nside_grid(c),
+                                                    nside_sched(c).n_multi, nside_long_red(c),
                                                     c.xchg + c.n + 8);
     CK(cudaGetLastError());
   }
@@ -1087,7 +1151,12 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     upload_sched(c->At, c->L.At, s);
     phase("schedules");
     c->grid_vec = vec_grid(*c, std::max<int64_t>(c->m, c->n));
-    c->grid_max = std::max({c->grid_a, c->grid_at, c->grid_vec});
+    // rank-independent n-side map (partitioned path): n and the device are
+    // the same on every rank, so is this grid
+    c->grid_nside = vec_grid(*c, c->n);
+    c->nside.thread_rows = 1;
+    c->nside.rows = c->n;
+    c->grid_max = std::max({c->grid_a, c->grid_at, c->grid_vec, c->grid_nside});
     for (double** p2 : {&c->part1, &c->part3, &c->partA, &c->partAt})
       *p2 = dev_alloc<double>(static_cast<size_t>(c->grid_max) * 16);
     c->hist = dev_alloc<double>(static_cast<size_t>(opt.block_limit));
@@ -1197,7 +1266,8 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->sm_count = c->sm_count;
     info->gather_l1 = (c->A.l1g ? 1 : 0) | (c->At.l1g ? 2 : 0);
     info->pdl = c->pdl ? 1 : 0;
-    info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0);
+    info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0) |
+                        (c->A.cta_row ? 4 : 0);
     info->resident = c->resident ? 1 : 0;
     info->segments = static_cast<int32_t>(std::max<size_t>(1, c->A.segs.size()) |
                                           (std::max<size_t>(1, c->At.segs.size()) << 16));
@@ -1323,9 +1393,9 @@ int rhp_power_step(rhp_ctx* c, double* vw, double* ww) {
       e.w = c->pw;
       e.in[0] = c->xchg;
       e.in[1] = c->pv;
-      epilogue_walk<EpiPowerDist><<<c->grid_at, kBlock, 0, c->stream>>>(fin(c->At).sched, e, c->partAt);
-      k_power_dist_finalize<<<1, kBlock, 0, c->stream>>>(c->ctl, c->partAt, c->grid_at,
-                                                         fin(c->At).sched.n_multi, fin(c->At).long_red);
+      epilogue_walk<EpiPowerDist><<<nside_grid(*c), kBlock, 0, c->stream>>>(nside_sched(*c), e, c->partAt);
+      k_power_dist_finalize<<<1, kBlock, 0, c->stream>>>(c->ctl, c->partAt, nside_grid(*c),
+                                                         nside_sched(*c).n_multi, nside_long_red(*c));
       CK(cudaGetLastError());
     }
     pull_ctl(*c);

@@ -383,6 +383,88 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   }
 }
 
+// Long-row engine (an operator made of few very long rows, e.g. C3's A:
+// 2000 rows of 1000 nonzeros; rhp_cuda.cu apply_engine_rule, every row
+// >= kCtaRowMin nonzeros). CTA b owns the contiguous rows [cta_row[b],
+// cta_row[b+1]) (balanced by nonzeros on the host) and walks them kCtaRowsBatch
+// at a time: thread t takes elements t, t + kBlock, ... of every row of the
+// batch (coalesced index / value loads, kCtaRowsBatch independent gather
+// chains per thread), then each row's partials are reduced by a fixed
+// shuffle tree per warp and a fixed warp order in shared memory, and lane q
+// of warp 0 runs row q's epilogue. No split rows, no tickets, no slots: the
+// operator's n_multi is 0, so the finalize reads only the CTA partials.
+// Deterministic (fixed element -> thread map and reduction order).
+template <class Epi, bool L1G = false>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_cta_rows(Csr A, const double* __restrict__ xg,
+                                                                    Sched s, const int32_t* cta_row,
+                                                                    Epi epi, double* part,
+                                                                    unsigned int* ticket) {
+  pdl_wait();
+  pdl_trigger();
+  if (!epi.enter()) return;
+  constexpr int RB = kCtaRowsBatch;
+  __shared__ double red[RB][kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[Epi::NRED];
+#pragma unroll
+  for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
+  const int64_t r0 = cta_row[blockIdx.x], r1 = cta_row[blockIdx.x + 1];
+  for (int64_t base = r0; base < r1; base += RB) {
+    int64_t lo[RB], hi[RB];
+    double p[RB];
+    int64_t len = 0;
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int64_t row = base + q;
+      lo[q] = row < r1 ? s.rp[row] : 0;
+      hi[q] = row < r1 ? s.rp[row + 1] : 0;
+      len = max(len, hi[q] - lo[q]);
+      p[q] = 0.0;
+    }
+    for (int64_t t = threadIdx.x; t < len; t += kBlock) {
+      int c[RB];
+      double v[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const bool ok = lo[q] + t < hi[q];
+        c[q] = ok ? __ldcs(A.ci + lo[q] + t) : 0;
+        v[q] = ok ? __ldcs(A.v + lo[q] + t) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < RB; ++q)
+        if (lo[q] + t < hi[q]) p[q] = fma(v[q], ld_gather<L1G>(xg + c[q]), p[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      double x = p[q];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+      if (lane == 0) red[q][warp] = x;
+    }
+    __syncthreads();
+    if (warp == 0 && lane < RB && base + lane < r1) {
+      const int64_t row = base + lane;
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) sum += red[lane][w];
+      if (s.seg_in) sum = add(__ldcg(s.seg_in + row), sum);
+      double ein[Epi::NIN > 0 ? Epi::NIN : 1];
+      load_inputs(epi, row, ein);
+      epi.row(row, sum, ein, 1, acc);
+    }
+    __syncthreads();  // red is rewritten by the next batch
+  }
+  if constexpr (Epi::REDUCE) {
+    block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
+    if constexpr (Epi::FINAL) {
+      if (elect_last_block(ticket)) {
+        epi.finalize(s, part, (int)gridDim.x);
+        if (threadIdx.x == 0) *ticket = 0u;
+      }
+    }
+  }
+}
+
 // Runs only the epilogue of spmv_fused<Epi>, with exactly its row -> lane
 // assignment (row sum argument 0, inputs read from global memory).
 template <class Epi>

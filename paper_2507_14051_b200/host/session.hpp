@@ -18,6 +18,20 @@ namespace rhpdhg {
 
 using Clock = std::chrono::steady_clock;
 
+namespace detail {
+// NVTX range for the duration of a scope (host/nvtx.cpp; header-only NVTX3,
+// no-op unless a profiler such as nsys / ncu --nvtx is attached). Names:
+// rhpdhg:setup / :ingest / :scaling / :power_iteration, :block, :kkt_check,
+// :restart, :finish.
+class NvtxRange {
+ public:
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace detail
+
 class Session {
  public:
   Session(const LpProblem& problem, const SolverConfig& cfg, const DeviceOptions& dopt);

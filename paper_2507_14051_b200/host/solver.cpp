@@ -130,6 +130,7 @@ Session::Session(const rhpdhg_lp_view& view, const std::string& name, bool valid
                  const SolverConfig& cfg, const DeviceOptions& dopt)
     : view_(view), name_(name), cfg_(cfg) {
   cfg.validate();
+  detail::NvtxRange setup_range("rhpdhg:setup");
   t0_ = Clock::now();
   // RHPDHG_SETUP_TRACE=1: per-phase setup times on stderr
   const bool trace = std::getenv("RHPDHG_SETUP_TRACE") != nullptr;
@@ -144,7 +145,10 @@ Session::Session(const rhpdhg_lp_view& view, const std::string& name, bool valid
   if (view.num_cons < 0 || view.num_vars < 0) throw UsageError("matrix dimensions must be nonnegative");
   // the matrix is validated by the device ingest (from_csr's exceptions),
   // then the vectors (LpProblem::validate, lp_problem.cpp:30-46)
-  dev_ = std::make_unique<detail::Device>(view, detail::options(dopt));
+  {
+    detail::NvtxRange r("rhpdhg:ingest");
+    dev_ = std::make_unique<detail::Device>(view, detail::options(dopt));
+  }
   rhp_ctx* c = dev_->get();
   if (!validated) detail::validate_vectors(view);
   // nonzeros after the ingest dropped explicit zeros (SparseMatrix::nnz())
@@ -161,12 +165,18 @@ Session::Session(const rhpdhg_lp_view& view, const std::string& name, bool valid
   }
   phase("device create+ingest");
   // (1) diagonal preconditioning on the device (solver.cpp:72-78)
-  detail::ok(rhp_scale(c, cfg.scaling_enabled ? 1 : 0, cfg.ruiz_iterations, cfg.pock_chambolle ? 1 : 0),
-             "rhp_scale");
+  {
+    detail::NvtxRange r("rhpdhg:scaling");
+    detail::ok(rhp_scale(c, cfg.scaling_enabled ? 1 : 0, cfg.ruiz_iterations, cfg.pock_chambolle ? 1 : 0),
+               "rhp_scale");
+  }
   phase("scaling");
   // (2) step size from the scaled norm (solver.cpp:81-88)
-  const PowerIterationResult pi = device_power_iteration(
-      c, n, nnz, cfg.power_tol, cfg.power_max_iters, cfg.power_seed);
+  PowerIterationResult pi;
+  {
+    detail::NvtxRange r("rhpdhg:power_iteration");
+    pi = device_power_iteration(c, n, nnz, cfg.power_tol, cfg.power_max_iters, cfg.power_seed);
+  }
   phase("power iteration");
   step_.matrix_norm_estimate = pi.value;
   step_.step_size = default_stepsize(pi.value, cfg.stepsize_multiplier);
@@ -206,6 +216,7 @@ Session::Session(const rhpdhg_lp_view& view, const std::string& name, bool valid
 Session::~Session() = default;
 
 KktResiduals Session::kkt_check(int which) {
+  detail::NvtxRange r("rhpdhg:kkt_check");
   rhp_kkt_sums s{};
   detail::ok(rhp_kkt(dev_->get(), which, &s), "rhp_kkt");
   spmv_counter::add(2);
@@ -234,7 +245,10 @@ bool Session::step() {
     return false;
   }
   rhp_block_out out{};
-  detail::ok(rhp_run_block(c, &out), "rhp_run_block");
+  {
+    detail::NvtxRange r("rhpdhg:block");
+    detail::ok(rhp_run_block(c, &out), "rhp_run_block");
+  }
   ++report_.device_blocks;
   if (out.breakdown)
     throw NumericalBreakdownError("canonical norm radicand " + std::to_string(out.q_last) +
@@ -262,6 +276,7 @@ bool Session::step() {
     }
   }
   if (out.verdict != 0) {  // do_restart (restart.cpp:71-83)
+    detail::NvtxRange r("rhpdhg:restart");
     step_.primal_weight = pid_update(pid_, std::sqrt(out.x_dist2), std::sqrt(out.y_dist2),
                                      std::sqrt(out.x_norm2), std::sqrt(out.y_norm2));
     const rhp_step dstep = device_step(step_, cfg_);
@@ -282,6 +297,7 @@ SolutionReport Session::finish() {
   while (step()) {
   }
   rhp_ctx* c = dev_->get();
+  detail::NvtxRange fin("rhpdhg:finish");
   if (status_ != SolveStatus::optimal) last_ = kkt_check(0);
   report_.loop_seconds = since(t_loop_);
   const Index m = view_.num_cons, n = view_.num_vars;

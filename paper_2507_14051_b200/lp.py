@@ -495,6 +495,7 @@ class Session:
                 "grid_vec": o[21], "sm_count": o[22],
                 "gather_l1": {"A": bool(o[23] & 1), "At": bool(o[23] & 2)}, "pdl": bool(o[24]),
                 "thread_rows": {"A": bool(o[25] & 1), "At": bool(o[25] & 2)},
+                "cta_rows": {"A": bool(o[25] & 4)},
                 "segments": {"A": int(o[26] & 0xffff), "At": int(o[26] >> 16)},
                 "resident": bool(o[27])}
 

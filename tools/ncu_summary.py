@@ -15,13 +15,17 @@ METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "dram_rd"),
     ("dram__bytes_write.sum", "dram_wr"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_%pk"),
+    # dram__throughput... is stored under a prefixed Triage name with empty
+    # values in `--page raw`; the per-direction percentages are populated
+    ("dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "dram_rd_%pk"),
+    ("dram__bytes_write.sum.pct_of_peak_sustained_elapsed", "dram_wr_%pk"),
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem_%pk"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2_%pk"),
     ("lts__t_sector_hit_rate.pct", "L2_hit%"),
     ("l1tex__t_sector_hit_rate.pct", "L1_hit%"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1_%pk"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue%"),
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "st_long"),

@@ -173,6 +173,15 @@ int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id);
  * calling this with its rank, solve one LP together. Device options are per
  * thread. */
 int rhpdhg_set_local_group(int rank, int world_size, const void* group);
+/* Directory benchmark (rhpdhg::run_benchmark, reference bench.cpp:171-266):
+ * solves every *.mps / *.mps.gz in `dir` on the GPU(s) (workers > 1: that
+ * many concurrent solves, worker w on GPU w % device_count), scores unsolved
+ * instances at their class time limit, writes the reference's JSON schema to
+ * json_path (if non-empty) and the per-instance table + SGM10 summary to
+ * `table` (NUL-terminated, truncated to table_cap). */
+int rhpdhg_run_benchmark(const char* dir, const rhpdhg_config_c* cfg, double small_limit_seconds,
+                         double large_limit_seconds, int workers, const char* json_path,
+                         char* table, int64_t table_cap);
 /* Small-LP cluster-resident device blocks: -1 auto (default), 0 off, 1 on. */
 int rhpdhg_set_resident(int mode);
 

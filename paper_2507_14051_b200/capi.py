@@ -200,7 +200,7 @@ CUDA_SYMBOLS = [
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",
     "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_set_distributed",
-    "rhpdhg_set_resident", "rhpdhg_set_local_group",
+    "rhpdhg_set_resident", "rhpdhg_set_local_group", "rhpdhg_run_benchmark",
     "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
@@ -298,6 +298,8 @@ def load_host() -> C.CDLL:
             "rhpdhg_set_device_options": [C.c_int, C.c_int, C.c_int64],
             "rhpdhg_set_distributed": [C.c_int, C.c_int, C.c_void_p],
             "rhpdhg_set_local_group": [C.c_int, C.c_int, C.c_void_p],
+            "rhpdhg_run_benchmark": [C.c_char_p, C.POINTER(ConfigC), C.c_double, C.c_double,
+                                     C.c_int, C.c_char_p, C.c_char_p, C.c_int64],
             "rhpdhg_set_resident": [C.c_int],
             "rhpdhg_session_create": [C.POINTER(LpView), C.POINTER(ConfigC), C.POINTER(P)],
             "rhpdhg_session_advance": [P, C.c_int64, C.POINTER(C.c_int32)],

@@ -366,16 +366,16 @@ __device__ __forceinline__ void iteration_sums(const double* part1, int grid1, c
 }
 
 // Last-block-done election. Returns true in exactly one block, after every
-// block's partial stores are visible to it.
+// block's partial stores are visible to it. The verdict travels through
+// __syncthreads_or (a register result), not a shared variable, so the
+// finalize's shared-memory trees that follow cannot race with its readers
+// (compute-sanitizer racecheck, tests/test_sanitizer.py).
 __device__ __forceinline__ bool elect_last_block(unsigned int* ticket) {
-  __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int t = atomicAdd(ticket, 1u);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
+  int mine = 0;
+  if (threadIdx.x == 0) mine = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  const bool last = __syncthreads_or(mine) != 0;
   if (last) __threadfence();
   return last;
 }

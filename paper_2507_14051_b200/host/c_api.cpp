@@ -2,6 +2,7 @@
 #include <cstring>
 #include <memory>
 #include <exception>
+#include <sstream>
 #include <string>
 
 #include "device.hpp"
@@ -9,6 +10,7 @@
 #include "rhpdhg/solver.hpp"
 #include "rhpdhg/mps.hpp"
 #include "rhpdhg/termination.hpp"
+#include "rhpdhg/bench.hpp"
 #include "rhpdhg_c.h"
 #include "session.hpp"
 
@@ -347,6 +349,30 @@ void fill_report(const SolutionReport& r, rhpdhg_report_c* out, double* x, doubl
 }  // namespace
 
 extern "C" {
+
+int rhpdhg_run_benchmark(const char* dir, const rhpdhg_config_c* cfg, double small_limit_seconds,
+                         double large_limit_seconds, int workers, const char* json_path,
+                         char* table, int64_t table_cap) {
+  return guarded([&] {
+    BenchmarkOptions opts;
+    opts.small_limit_seconds = small_limit_seconds;
+    opts.large_limit_seconds = large_limit_seconds;
+    opts.workers = workers;
+    const SolverConfig c = to_config(cfg);
+    std::ostringstream log;
+    const BenchmarkReport rep = run_benchmark(dir, c, opts, &log);
+    if (json_path && *json_path) write_benchmark_json(rep, c.epsilon, json_path);
+    std::ostringstream os;
+    os << log.str();
+    write_benchmark_table(rep, os);
+    if (table && table_cap > 0) {
+      const std::string t = os.str();
+      const size_t k = std::min<size_t>(t.size(), static_cast<size_t>(table_cap - 1));
+      std::memcpy(table, t.data(), k);
+      table[k] = '\0';
+    }
+  });
+}
 
 int rhpdhg_kkt_residuals(const rhpdhg_lp_view* lp, const double* x, const double* y,
                          rhpdhg_kkt_c* out) {

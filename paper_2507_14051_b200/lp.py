@@ -366,6 +366,22 @@ def write_mps(lp: LpProblem, path: str) -> None:
         f.write("\n".join(lines) + "\n")
 
 
+def run_benchmark(directory: str, cfg: SolverConfig | None = None,
+                  small_limit_seconds: float = 3600.0, large_limit_seconds: float = 18000.0,
+                  workers: int = 1, json_path: str | None = None) -> str:
+    """rhpdhg::run_benchmark over a directory of *.mps / *.mps.gz on the GPU(s)
+    (reference bench.cpp:171-266): returns the per-instance table with the
+    SGM10 summary; writes the reference's JSON report to json_path."""
+    lib = capi.load_host()
+    cc = (cfg or SolverConfig()).to_c()
+    buf = C.create_string_buffer(1 << 20)
+    raise_status(lib.rhpdhg_run_benchmark(str(directory).encode(), C.byref(cc),
+                                          small_limit_seconds, large_limit_seconds, workers,
+                                          (json_path or "").encode(), buf, len(buf)),
+                 lib.rhpdhg_last_error().decode(errors="replace"))
+    return buf.value.decode(errors="replace")
+
+
 def set_device_options(device: int = 0, use_graph: bool = True, block_limit: int = 64) -> None:
     lib = capi.load_host()
     raise_status(lib.rhpdhg_set_device_options(device, int(use_graph), block_limit),

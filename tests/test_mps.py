@@ -162,3 +162,31 @@ def test_parallel_reader_equals_sequential_reader(tmp_path, monkeypatch):
             same_lp(got, want)
             assert gw == ww, path
     assert werr is not None and "duplicate entry" in werr  # the last variant
+
+
+@pytest.mark.gpu
+def test_gpu_directory_benchmark_sgm10(gpu, tmp_path):
+    """rhpdhg::run_benchmark on the GPU (bench.cpp:171-266): analytic LPs plus
+    a broken file, the reference's JSON schema, SGM10 rows; 2 workers."""
+    import json
+
+    from paper_2507_14051_b200.lp import run_benchmark
+
+    for inst in ANALYTIC[:4]:
+        lp = support.lp_from_json(inst["lp"])
+        lp.maximization = False
+        write_mps(lp, tmp_path / f"{inst['name']}.mps")
+    (tmp_path / "broken.mps").write_text("NAME broken\nROWS\nGARBAGE\n")
+    out = tmp_path / "report.json"
+    for workers in (1, 2):
+        table = run_benchmark(str(tmp_path), workers=workers, small_limit_seconds=30.0,
+                              json_path=str(out))
+        d = json.loads(out.read_text())
+        assert d["schema_version"] == 1 and len(d["records"]) == 5
+        assert d["records"][0]["instance"] == "boxonly" or d["records"][0]["status"] in (
+            "optimal", "error")
+        st = {r["instance"]: r["status"] for r in d["records"]}
+        assert st["broken"] == "error" and sum(v == "optimal" for v in st.values()) == 4
+        assert [s["group"] for s in d["summary"]] == ["small", "medium", "large", "total"]
+        assert d["summary"][3]["count"] == 5 and d["summary"][3]["solved"] == 4
+        assert "SGM10" in table

@@ -2,7 +2,7 @@
 #   make            -> paper_2507_14051_b200/lib/librhp_cuda.so, librhpdhg.so, oracle/liboracle.so
 #   make ref        -> oracle/_ref/librhpdhg_ref.so (needs /root/reference; test infrastructure)
 NVCC     ?= /usr/local/cuda/bin/nvcc
-CXX      ?= g++
+CXX      := /usr/bin/g++  # the system toolchain nvcc also uses (one libstdc++ per process)
 PKG      := paper_2507_14051_b200
 LIB      := $(PKG)/lib
 ARCH     := -gencode arch=compute_100a,code=sm_100a

@@ -175,6 +175,7 @@ struct Ctl {
   int32_t k1_token_pending;        // row-partitioned path: K1 ran, control not yet
   double* hist;                    // [block_limit] residual history of the current block
   int* stop_mirror;                // partitioned plain mode: mapped host flags [block_limit]
+  unsigned long long peer_epoch;   // peer exchange sequence (peer.cuh): only grows
 };
 
 // Operator schedule (built by layout.cu for a given warp count): chunk c is

@@ -343,6 +343,28 @@ struct EpiStore {
   __device__ void finalize(const Sched&, const double*, int) {}
 };
 
+// Intermediate column segment of a segmented operator (rhp_cuda.cu
+// launch_spmv): stores its row sums like EpiStore, but runs only when the
+// final segment's epilogue `Gate` will (same enter() test, evaluated on a
+// copy), so iterations past a block's stop skip every segment pass, not just
+// the last.
+template <class Gate>
+struct EpiSegStore {
+  static constexpr int NRED = 1;
+  static constexpr int NIN = 0;
+  static constexpr bool REDUCE = false;
+  static constexpr bool FINAL = false;
+  double* out;
+  const double* in[1];
+  Gate gate;
+  __device__ bool enter() {
+    Gate g = gate;
+    return g.enter();
+  }
+  __device__ void row(int64_t i, double s, const double*, int, double (&)[NRED]) { out[i] = s; }
+  __device__ void finalize(const Sched&, const double*, int) {}
+};
+
 // w = A^T (A v): store w, reduce v.w and w.w (pdhg.cpp:141-146); input: v
 struct EpiPowerW {
   static constexpr int NRED = 2;

@@ -83,15 +83,20 @@ __device__ __forceinline__ void owned_slice(const PeerView& v, int r, int64_t* l
   *hi = v.n * (r + 1) / v.world;
 }
 
-__global__ void k_peer_signal(const Ctl* ctl, int token, PeerView v) {
+// The flag sequence number is the context's exchange epoch: a counter that
+// only grows (one step per exchange, in lockstep on every rank) and that
+// rhp_reset_iterate / the benchmark kernel timers never rewind — unlike the
+// iteration total, which a reset sets back to 0 while the peers' flag words
+// still hold the old, larger values.
+__global__ void k_peer_signal(Ctl* ctl, int token, PeerView v) {
   if (!peer_enter(ctl, token)) return;
-  if (threadIdx.x == 0) peer_signal(v, 0, static_cast<unsigned long long>(ctl->total) + 1);
+  if (threadIdx.x == 0) peer_signal(v, 0, ++ctl->peer_epoch);
 }
 
 __global__ void __launch_bounds__(kBlock) k_peer_reduce(const Ctl* ctl, int token, PeerView v,
                                                         unsigned int* ticket) {
   if (!peer_enter(ctl, token)) return;
-  const unsigned long long seq = static_cast<unsigned long long>(ctl->total) + 1;
+  const unsigned long long seq = ctl->peer_epoch;  // set by k_peer_signal (same stream)
   peer_wait(v, 0, seq);
   int64_t lo, hi;
   owned_slice(v, v.rank, &lo, &hi);
@@ -109,11 +114,11 @@ __global__ void __launch_bounds__(kBlock) k_peer_reduce(const Ctl* ctl, int toke
   }
   // last CTA to finish signals phase 2 (every CTA's slice stores fenced at
   // system scope first, so a peer's acquire of the signal sees all of them)
-  __shared__ bool last;
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
+  int mine = 0;
+  if (threadIdx.x == 0) mine = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  const bool last = __syncthreads_or(mine) != 0;
   if (last && threadIdx.x == 0) {
     *ticket = 0u;
     peer_signal(v, 1, seq);
@@ -122,7 +127,7 @@ __global__ void __launch_bounds__(kBlock) k_peer_reduce(const Ctl* ctl, int toke
 
 __global__ void __launch_bounds__(kBlock) k_peer_gather(const Ctl* ctl, int token, PeerView v) {
   if (!peer_enter(ctl, token)) return;
-  const unsigned long long seq = static_cast<unsigned long long>(ctl->total) + 1;
+  const unsigned long long seq = ctl->peer_epoch;
   peer_wait(v, 1, seq);
   double* local = v.xchg[v.rank];
   for (int r = 0; r < v.world; ++r) {

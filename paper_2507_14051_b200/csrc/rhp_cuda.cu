@@ -398,8 +398,11 @@ void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const 
     launch_one(c, op, grid, xg, epi, part, ticket, s);
     return;
   }
+  EpiSegStore<Epi> seg{};
+  seg.out = op.segbuf;
+  seg.gate = epi;
   for (size_t k = 0; k + 1 < op.segs.size(); ++k)
-    launch_one(c, op.segs[k], grid, xg, store_into(op.segbuf), nullptr, nullptr, s);
+    launch_one(c, op.segs[k], grid, xg, seg, nullptr, nullptr, s);
   launch_one(c, op.segs.back(), grid, xg, epi, part, ticket, s);
 }
 

@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstdint>
 #include <memory>
@@ -44,10 +45,24 @@ struct Comm {
   virtual void allreduce(double* buf, size_t count, bool max, cudaStream_t s) = 0;
   virtual void allreduce_max_i64(int64_t* buf, size_t count, cudaStream_t s) = 0;
   // recv = concatenation of every rank's `bytes` of send, in rank order
+  // (send may be recv + rank * bytes: in place)
   virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  // recv[0..chunk) = sum over ranks of send[rank * chunk .. (rank + 1) * chunk)
+  virtual void reduce_scatter(const double* send, double* recv, size_t chunk, cudaStream_t s) = 0;
   // peer-memory exchange needs an NCCL communicator for the IPC handles
   virtual bool is_nccl() const { return false; }
 };
+
+// Rank-ordered sums of chunk `r` of P device buffers (reduce-scatter).
+__global__ void k_local_reduce_chunk(double* out, const double* const* in, int P, size_t chunk,
+                                     size_t offset) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < chunk;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double v = in[0][offset + i];
+    for (int q = 1; q < P; ++q) v += in[q][offset + i];
+    out[i] = v;
+  }
+}
 
 // Rank-ordered elementwise reduction of P device buffers.
 template <class T>
@@ -110,11 +125,24 @@ class LocalComm final : public Comm {
   }
   void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
     publish(send, s);
-    for (int q = 0; q < g_->world; ++q)
-      if (bytes)
-        ck(cudaMemcpyAsync(static_cast<char*>(recv) + q * bytes, g_->ptrs[q], bytes,
-                           cudaMemcpyDeviceToDevice, s));
+    for (int q = 0; q < g_->world; ++q) {
+      char* dst = static_cast<char*>(recv) + q * bytes;
+      if (bytes && dst != g_->ptrs[q])  // in place: the own chunk is already there
+        ck(cudaMemcpyAsync(dst, g_->ptrs[q], bytes, cudaMemcpyDeviceToDevice, s));
+    }
     finish(s);
+  }
+  void reduce_scatter(const double* send, double* recv, size_t chunk, cudaStream_t s) override {
+    ensure_scratch(chunk * sizeof(double));
+    publish(send, s);
+    ck(cudaMemcpyAsync(dptrs_, g_->ptrs.data(), sizeof(void*) * g_->world, cudaMemcpyHostToDevice, s));
+    const int grid = static_cast<int>(std::min<size_t>(1024, (chunk + 255) / 256 + 1));
+    k_local_reduce_chunk<<<grid, 256, 0, s>>>(static_cast<double*>(scratch_),
+                                             reinterpret_cast<const double* const*>(dptrs_),
+                                             g_->world, chunk, chunk * rank_);
+    ck(cudaGetLastError());
+    finish(s);
+    if (chunk) ck(cudaMemcpyAsync(recv, scratch_, chunk * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
 
  private:
@@ -134,14 +162,17 @@ class LocalComm final : public Comm {
     for (int q = 0; q < g_->world; ++q)
       if (q != rank_) ck(cudaStreamWaitEvent(s, g_->done[q], 0));
   }
-  template <class T>
-  void reduce(T* buf, size_t count, bool max, cudaStream_t s) {
-    if (count * sizeof(T) > scratch_bytes_) {
+  void ensure_scratch(size_t bytes) {
+    if (bytes > scratch_bytes_) {
       if (scratch_) ck(cudaFree(scratch_));
-      scratch_bytes_ = count * sizeof(T) + 64;
+      scratch_bytes_ = bytes + 64;
       ck(cudaMalloc(&scratch_, scratch_bytes_));
     }
     if (!dptrs_) ck(cudaMalloc(&dptrs_, sizeof(void*) * g_->world));
+  }
+  template <class T>
+  void reduce(T* buf, size_t count, bool max, cudaStream_t s) {
+    ensure_scratch(count * sizeof(T));
     publish(buf, s);
     // pointers of this collective, snapshotted for the kernel (pageable
     // source: the copy completes before cudaMemcpyAsync returns)

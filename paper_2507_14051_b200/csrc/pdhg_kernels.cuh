@@ -232,17 +232,25 @@ struct EpiDual {
 // After the allreduce of [A_p^T y+_p partials (n) | y-side sums (5)]:
 // one CTA reduces the (replicated, rank-identical) x-side partials and runs
 // the control on the global sums.
+// xsums: the allreduced y-side sums (5); x_sums (sharded path): the
+// allreduced x-side sums (4) of the previous n-side walk, else they are
+// reduced here from the (rank-identical) walker partials part3.
 __global__ void __launch_bounds__(kBlock) k_dist_control(Ctl* ctl, const double* part3, int grid3,
                                                          int n_multi3, const double* long_red3,
-                                                         const double* xsums, int token) {
+                                                         const double* xsums, int token,
+                                                         const double* x_sums) {
   if (!ctl->graph_mode && ctl->k1_token_pending != token && !ctl->bench) {
     // an iteration past the block's stop: tell the host (rhp_run_block polls)
     if (threadIdx.x == 0 && ctl->stop_mirror) reinterpret_cast<volatile int*>(ctl->stop_mirror)[token] = 1;
     return;
   }
   double t3[4];
-  block_sum_partials<4>(part3, grid3, grid3, t3);
-  add_slots<4>(long_red3, n_multi3, t3);
+  if (x_sums) {
+    for (int q = 0; q < 4; ++q) t3[q] = __ldcg(x_sums + q);
+  } else {
+    block_sum_partials<4>(part3, grid3, grid3, t3);
+    add_slots<4>(long_red3, n_multi3, t3);
+  }
   if (threadIdx.x == 0) {
     double t1[5];
     for (int q = 0; q < 5; ++q) t1[q] = __ldcg(xsums + q);
@@ -579,6 +587,39 @@ __global__ void __launch_bounds__(kBlock) k_power_dist_finalize(Ctl* ctl, const 
     ctl->pw_vw = t[0];
     ctl->pw_ww = t[1];
   }
+}
+
+// ------------------------------------------------ sharded (Option B) helpers --
+// One CTA: the N walker partials (fixed order) into out[0..N), this rank's
+// share of the scalars the next allreduce sums.
+template <int N>
+__global__ void __launch_bounds__(kBlock) k_sum_partials(const double* part, int grid, double* out) {
+  double t[N];
+  block_sum_partials<N>(part, grid, grid, t);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < N; ++q) out[q] = t[q];
+}
+
+// The KKT sums from the allreduced scalars: row side s[0..4), column side
+// s[4..10) (layout of EpiKktRowDist / EpiKktCol partials).
+__global__ void k_kkt_from_sums(Ctl* ctl, const double* s) {
+  if (threadIdx.x != 0) return;
+  ctl->kkt_nan_y = __ldcg(s + 0);
+  ctl->kkt_viol2 = __ldcg(s + 1);
+  ctl->kkt_py_inf = __ldcg(s + 2);
+  ctl->kkt_py = __ldcg(s + 3);
+  ctl->kkt_nan_x = __ldcg(s + 4);
+  ctl->kkt_pr_inf = __ldcg(s + 5);
+  ctl->kkt_pr = __ldcg(s + 6);
+  ctl->kkt_eq2 = __ldcg(s + 7);
+  ctl->kkt_cone2 = __ldcg(s + 8);
+  ctl->kkt_cx = __ldcg(s + 9);
+}
+
+__global__ void k_power_from_sums(Ctl* ctl, const double* s) {
+  if (threadIdx.x != 0) return;
+  ctl->pw_vw = __ldcg(s + 0);
+  ctl->pw_ww = __ldcg(s + 1);
 }
 
 }  // namespace rhp

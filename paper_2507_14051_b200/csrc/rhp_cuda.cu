@@ -59,6 +59,7 @@ struct NcclApi {
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclReduceScatter) ReduceScatter = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -72,9 +73,11 @@ const NcclApi& nccl() {
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(dlsym(h, "ncclReduceScatter"));
     return a;
   }();
-  if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllReduce || !api.AllGather)
+  if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllReduce || !api.AllGather ||
+      !api.ReduceScatter)
     throw rhp::DeviceFailure("NCCL (libnccl.so.2) not found: the row-partitioned path needs it");
   return api;
 }
@@ -102,6 +105,10 @@ class NcclComm final : public rhp::Comm {
   void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
     if (nccl().AllGather(send, recv, bytes, ncclChar, comm_, s) != ncclSuccess)
       throw CudaError("ncclAllGather failed");
+  }
+  void reduce_scatter(const double* send, double* recv, size_t chunk, cudaStream_t s) override {
+    if (nccl().ReduceScatter(send, recv, chunk, ncclDouble, ncclSum, comm_, s) != ncclSuccess)
+      throw CudaError("ncclReduceScatter failed");
   }
   bool is_nccl() const override { return true; }
 
@@ -158,6 +165,10 @@ struct DevOp : DeviceCsr {
   double* segbuf = nullptr;  // [rows] running row sums of the segments
   // long-row engine (spmv_cta_rows): CTA b owns rows [cta_row[b], cta_row[b+1])
   int32_t* cta_row = nullptr;
+  // column segments: the row band [seg_rb, seg_re) split by columns; an
+  // intermediate segment stores its band-local row sums at seg_out
+  int64_t seg_rb = 0, seg_re = 0;
+  double* seg_out = nullptr;
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
 
@@ -193,6 +204,19 @@ struct rhp_ctx {
   // and desynchronise the collectives).
   Sched nside{};
   int grid_nside = 1;
+  // Option B of SURVEY.md §8(e) ("sharded", the default at world > 1 without
+  // the peer exchange; RHP_DIST_REPLICATED=1 keeps Option A): rank r owns
+  // the column slice [nlo, nhi) = [r S, min((r+1) S, n)), S = ceil(n/P).
+  // Per iteration: A_p^T y+_p (all n) is reduce-scattered to the owners,
+  // the y-side sums of K1 and the x-side sums of the previous n-side walk go
+  // through one 9-scalar allreduce, every rank runs the control on the same
+  // sums, walks ONLY its slice (aty update + next primal step), and x+ is
+  // all-gathered. Same bytes as the allreduce of Option A, n-side work 1/P.
+  bool sharded = false;
+  int64_t S = 0, nlo = 0, nhi = 0, nalloc = 0;  // nalloc = max(n, P S): padded n-vectors
+  double* rsb = nullptr;   // [S] owned slice of the reduce-scattered A^T partial
+  double* dsum = nullptr;  // [16] per-iteration scalars: y-side 0..4, x-side 5..8
+  double* ksum = nullptr;  // [16] KKT scalars (row 0..3, col 4..9) / power dots (0..1)
   // CUDA graph of one block of iterations
   bool graph_built = false;
   cudaGraph_t graph = nullptr;
@@ -399,10 +423,11 @@ void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const 
     return;
   }
   EpiSegStore<Epi> seg{};
-  seg.out = op.segbuf;
   seg.gate = epi;
-  for (size_t k = 0; k + 1 < op.segs.size(); ++k)
+  for (size_t k = 0; k + 1 < op.segs.size(); ++k) {
+    seg.out = op.segs[k].seg_out;
     launch_one(c, op.segs[k], grid, xg, seg, nullptr, nullptr, s);
+  }
   launch_one(c, op.segs.back(), grid, xg, epi, part, ticket, s);
 }
 
@@ -528,17 +553,30 @@ __global__ void k_popcount(const unsigned int* bits, int64_t words, unsigned lon
 // one band of W consecutive chunks at a time): the distinct 32-B sectors of
 // the gathered vector touched by a band, times 32 B, maximised over up to 8
 // bands spread over the operator. Deterministic (structure only).
-double band_footprint_bytes(rhp_ctx& c, const DevOp& d, const HostOperator& h, int64_t cols) {
-  const int64_t W = h.sched.n_warps, chunks = h.sched.n_chunks;
-  if (W <= 0 || chunks <= W) return static_cast<double>(cols) * 8.0;  // one band: the whole operator
+// Gather footprint of the bands of an operator: band b = the W consecutive
+// merge-path chunks the whole grid walks at once (chunks bW .. bW+W-1), its
+// footprint = distinct 32-B sectors of the gathered vector its nonzeros
+// touch. Bands whose footprint exceeds `limit` gather mostly from DRAM. Up to
+// 256 bands are measured (evenly spaced when there are more); the hull of
+// the rows of the bad bands (each measured band standing for the rows up to
+// its measured neighbours) is returned in [rb, re). False if none is bad.
+bool bad_band_hull(rhp_ctx& c, const DevOp& d, const HostOperator& h, int64_t cols, double limit,
+                   int64_t* rb, int64_t* re) {
+  const int64_t W = h.sched.n_warps, chunks = h.sched.n_chunks, rows = h.rows;
+  *rb = 0;
+  *re = rows;
+  if (W <= 0 || chunks <= W) return static_cast<double>(cols) * 8.0 > limit;  // one band
   const int64_t bands = chunks / W;
   const int64_t words = (cols / 4) / 32 + 2;
   unsigned int* bits = dev_alloc<unsigned int>(static_cast<size_t>(words));
   unsigned long long* total = dev_alloc<unsigned long long>(1);
-  double worst = 0.0;
-  const int64_t samples = std::min<int64_t>(8, bands);
+  const int64_t samples = std::min<int64_t>(256, bands);
+  std::vector<int64_t> band_of(static_cast<size_t>(samples));
+  std::vector<char> bad(static_cast<size_t>(samples), 0);
+  auto band_row = [&](int64_t b) { return h.warp_row[std::min(chunks, b * W)]; };
   for (int64_t k = 0; k < samples; ++k) {
     const int64_t b = bands * k / samples;
+    band_of[k] = b;
     const int64_t lo = h.warp_nz[b * W], hi = h.warp_nz[std::min(chunks, (b + 1) * W)];
     CK(cudaMemsetAsync(bits, 0, words * sizeof(unsigned int), c.stream));
     CK(cudaMemsetAsync(total, 0, sizeof(unsigned long long), c.stream));
@@ -547,11 +585,24 @@ double band_footprint_bytes(rhp_ctx& c, const DevOp& d, const HostOperator& h, i
     unsigned long long t = 0;
     CK(cudaMemcpyAsync(&t, total, sizeof(t), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
-    worst = std::max(worst, 32.0 * static_cast<double>(t));
+    bad[k] = 32.0 * static_cast<double>(t) > limit;
   }
   cudaFree(bits);
   cudaFree(total);
-  return worst;
+  int64_t first = -1, last = -1;
+  for (int64_t k = 0; k < samples; ++k)
+    if (bad[k]) {
+      if (first < 0) first = k;
+      last = k;
+    }
+  if (first < 0) return false;
+  *rb = first == 0 ? 0 : band_row(band_of[first - 1] + 1);
+  *re = last == samples - 1 ? rows : band_row(band_of[last + 1]);
+  if (*re <= *rb) {
+    *rb = 0;
+    *re = rows;
+  }
+  return true;
 }
 
 // Column segments (segments.cuh) of an operator whose gathered vector is
@@ -575,27 +626,48 @@ void build_segments(rhp_ctx& c, DevOp& d, const HostOperator& h, int64_t cols, i
   const int64_t S = static_cast<int64_t>(std::ceil(static_cast<double>(cols) * 8.0 / seg_bytes));
   if (S <= 1) return;
   const char* force = std::getenv("RHP_SEG_FORCE");
-  if (!(force && force[0] == '1') && band_footprint_bytes(c, d, h, cols) <= seg_bytes) return;
+  int64_t rb = 0, re = d.rows;
+  if (!(force && force[0] == '1') && !bad_band_hull(c, d, h, cols, seg_bytes, &rb, &re)) return;
+  // RHP_SEG_BAND=0: split every row (the pre-band behaviour), for A/B runs;
+  // RHP_SEG_BAND=<lo>,<hi>: that row band (tests, with RHP_SEG_FORCE=1)
+  if (const char* e = std::getenv("RHP_SEG_BAND")) {
+    long long lo = 0, hi = 0;
+    if (std::sscanf(e, "%lld,%lld", &lo, &hi) == 2) {
+      rb = std::max<int64_t>(0, std::min<int64_t>(lo, d.rows));
+      re = std::max<int64_t>(rb, std::min<int64_t>(hi, d.rows));
+    } else if (e[0] == '0') {
+      rb = 0;
+      re = d.rows;
+    }
+  }
   std::vector<int32_t> cb(static_cast<size_t>(S) + 1);
   for (int64_t k = 0; k <= S; ++k) cb[k] = static_cast<int32_t>(cols * k / S);
   std::vector<DeviceCsr> parts;
   std::vector<std::vector<int64_t>> hrp;
-  split_columns(d, cb, parts, hrp, c.stream);
+  split_columns(d, cb, rb, re, parts, hrp, c.stream);
+  // running row sums: zero outside the band for good (only the band's rows
+  // pass through the intermediate segments)
   d.segbuf = dev_alloc<double>(static_cast<size_t>(d.rows));
+  d.seg_rb = rb;
+  d.seg_re = re;
   d.segs.resize(static_cast<size_t>(S));
   for (int64_t k = 0; k < S; ++k) {
     DevOp& g = d.segs[k];
+    const bool last = k == S - 1;
     static_cast<DeviceCsr&>(g) = parts[k];
-    HostOperator h;
-    h.rows = d.rows;
-    h.cols = cb[k + 1] - cb[k];
-    h.nnz = parts[k].nnz;
-    h.rp = std::move(hrp[k]);
-    build_schedule(h, static_cast<int64_t>(grid) * kWarps, kRowWeight);
-    upload_sched(g, h, c.stream);
-    apply_engine_rule(g, h.rp);
+    HostOperator hs;
+    hs.rows = parts[k].rows;
+    hs.cols = last ? cols : cb[k + 1] - cb[k];
+    hs.nnz = parts[k].nnz;
+    hs.rp = std::move(hrp[k]);
+    build_schedule(hs, static_cast<int64_t>(grid) * kWarps, kRowWeight);
+    upload_sched(g, hs, c.stream);
+    apply_engine_rule(g, hs.rp);
     g.l1g = d.l1g;
-    g.sched.seg_in = k == 0 ? nullptr : d.segbuf;
+    // intermediate segments read and write the band's slice of the running
+    // sums (local row r -> segbuf[rb + r]); the last one reads every row's
+    g.sched.seg_in = k == 0 ? nullptr : (last ? d.segbuf : d.segbuf + rb);
+    g.seg_out = last ? nullptr : d.segbuf + rb;
   }
 }
 
@@ -705,6 +777,8 @@ void allreduce_max(rhp_ctx& c, double* buf, size_t count, cudaStream_t s) {
   c.comm->allreduce(buf, count, true, s);
 }
 
+void launch_iteration_sharded(rhp_ctx& c, int token, cudaStream_t s);
+
 void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false) {
   if (!c.dist) {
     EpiDual d = epi_dual(c, token);
@@ -714,8 +788,13 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
     launch_spmv(c, c.At, c.grid_at, c.yp, a, c.part3, nullptr, s);
     return;
   }
-  // row-partitioned: local A x+ with the dual epilogue (y-side sums -> xchg[n..]),
-  // local A_p^T y+_p -> xchg[0..n), one allreduce, control, aty/primal epilogue
+  if (c.sharded) {
+    launch_iteration_sharded(c, token, s);
+    return;
+  }
+  // row-partitioned, Option A: local A x+ with the dual epilogue (y-side sums
+  // -> xchg[n..]), local A_p^T y+_p -> xchg[0..n), one allreduce, control,
+  // aty/primal epilogue over all n columns (replicated)
   EpiDual d = epi_dual(c, token);
   d.xchg = c.xchg + c.n;
   launch_spmv(c, c.A, c.grid_a, c.xp, d, c.part1, &c.ctl->ticket_dual, s);
@@ -732,7 +811,7 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
     allreduce(c, c.xchg, static_cast<size_t>(c.n) + 5, s);
   }
   k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, nside_grid(c), nside_sched(c).n_multi,
-                                      nside_long_red(c), c.xchg + c.n, token);
+                                      nside_long_red(c), c.xchg + c.n, token, nullptr);
   CK(cudaGetLastError());
   EpiAtyDist e{};
   e.ctl = c.ctl;
@@ -743,6 +822,43 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   e.token = token;
   epilogue_walk<EpiAtyDist><<<nside_grid(c), kBlock, 0, s>>>(nside_sched(c), e, c.part3);
   CK(cudaGetLastError());
+}
+
+// Sharded n-side walk epilogue tail: this rank's x-side sums of the walk
+// into dsum[5..9) (summed across ranks by the next iteration's allreduce),
+// then every rank's x+ slice to every rank (in-place all-gather).
+void sharded_walk_tail(rhp_ctx& c, cudaStream_t s) {
+  k_sum_partials<4><<<1, kBlock, 0, s>>>(c.part3, c.grid_nside, c.dsum + 5);
+  CK(cudaGetLastError());
+  c.comm->allgather(c.xp + c.nlo, c.xp, static_cast<size_t>(c.S) * sizeof(double), s);
+}
+
+// One iteration of the sharded partitioned path (Option B, rhp_ctx::sharded).
+void launch_iteration_sharded(rhp_ctx& c, int token, cudaStream_t s) {
+  const int64_t lo = c.nlo;
+  EpiDual d = epi_dual(c, token);
+  d.xchg = c.dsum;  // y-side sums -> dsum[0..5)
+  launch_spmv(c, c.A, c.grid_a, c.xp, d, c.part1, &c.ctl->ticket_dual, s);
+  EpiStore st = store_into(c.xchg);
+  st.ctl = c.ctl;
+  st.token = token;
+  launch_spmv(c, c.At, c.grid_at, c.yp, st, nullptr, nullptr, s);
+  c.comm->reduce_scatter(c.xchg, c.rsb, static_cast<size_t>(c.S), s);
+  allreduce(c, c.dsum, 9, s);  // y-side (this iteration) + x-side (previous walk) sums
+  k_dist_control<<<1, kBlock, 0, s>>>(c.ctl, c.part3, c.grid_nside, 0, nullptr, c.dsum, token,
+                                      c.dsum + 5);
+  CK(cudaGetLastError());
+  EpiAtyDist e{};
+  e.ctl = c.ctl;
+  e.aty = c.aty + lo;
+  e.o = PrimalOut{c.x + lo, c.xp + lo};
+  const double* in[] = {c.rsb, c.aty + lo, c.aty0 + lo, c.x + lo, c.c + lo, c.vl + lo, c.vu + lo,
+                        c.x0 + lo};
+  for (int k = 0; k < EpiAtyDist::NIN; ++k) e.in[k] = in[k];
+  e.token = token;
+  epilogue_walk<EpiAtyDist><<<c.grid_nside, kBlock, 0, s>>>(c.nside, e, c.part3);
+  CK(cudaGetLastError());
+  sharded_walk_tail(c, s);
 }
 
 // Contiguous split of an operator's rows into `parts` runs balanced by
@@ -851,13 +967,15 @@ void launch_resident(rhp_ctx& c, cudaStream_t s) {
 }
 
 void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
+  const int64_t lo = c.sharded ? c.nlo : 0;  // sharded: the owned slice only
   EpiPrimal e{};
   e.ctl = c.ctl;
-  e.o = primal_out(c);
-  const double* in[] = {c.aty, c.x, c.c, c.vl, c.vu, c.x0};
+  e.o = PrimalOut{c.x + lo, c.xp + lo};
+  const double* in[] = {c.aty + lo, c.x + lo, c.c + lo, c.vl + lo, c.vu + lo, c.x0 + lo};
   for (int k = 0; k < EpiPrimal::NIN; ++k) e.in[k] = in[k];
   epilogue_walk<EpiPrimal><<<nside_grid(c), kBlock, 0, s>>>(nside_sched(c), e, c.part3);
   CK(cudaGetLastError());
+  if (c.sharded) sharded_walk_tail(c, s);
 }
 
 void build_graph(rhp_ctx& c) {
@@ -942,6 +1060,32 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
   ec.long_red_row = fin(c.A).long_red;
   if (!c.dist) {
     launch_spmv(c, c.At, c.grid_at, ys, ec, c.partAt, &c.ctl->ticket_kkt, c.stream);
+  } else if (c.sharded) {
+    // Option B: x needs all its slices for A_p x; the column side runs on the
+    // owned slice of the reduce-scattered A^T y; row (0..3) and column
+    // (4..9) sums meet in one 10-scalar allreduce
+    cudaStream_t s = c.stream;
+    const int64_t lo = c.nlo;
+    if (xs == c.x) c.comm->allgather(c.x + lo, c.x, static_cast<size_t>(c.S) * sizeof(double), s);
+    EpiKktRowDist rd{};
+    static_cast<EpiKktRow&>(rd) = er;
+    rd.xsums = c.ksum;
+    launch_spmv(c, c.A, c.grid_a, xs, rd, c.partA, &c.ctl->ticket_kkt, s);
+    launch_spmv(c, c.At, c.grid_at, ys, store_into(c.xchg), nullptr, nullptr, s);
+    c.comm->reduce_scatter(c.xchg, c.rsb, static_cast<size_t>(c.S), s);
+    EpiKktColDist cd{};
+    cd.col = ec;
+    cd.col.aty_refresh = refresh ? c.aty + lo : nullptr;
+    cd.col.xout = write_out ? c.xout + lo : nullptr;
+    cd.col.rcout = write_out ? c.rcout + lo : nullptr;
+    const double* in[] = {c.rsb, xs + lo, c.cs + lo, c.co + lo, c.vlo + lo, c.vuo + lo};
+    for (int k = 0; k < EpiKktColDist::NIN; ++k) cd.in[k] = in[k];
+    epilogue_walk<EpiKktColDist><<<c.grid_nside, kBlock, 0, s>>>(c.nside, cd, c.partAt);
+    k_sum_partials<6><<<1, kBlock, 0, s>>>(c.partAt, c.grid_nside, c.ksum + 4);
+    CK(cudaGetLastError());
+    allreduce(c, c.ksum, 10, s);
+    k_kkt_from_sums<<<1, 32, 0, s>>>(c.ctl, c.ksum);
+    CK(cudaGetLastError());
   } else {
     // local rows; the last block publishes the row-side sums into xchg[n+8..n+12)
     EpiKktRowDist rd{};
@@ -1081,6 +1225,11 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     c->dist = opt.nccl_id != nullptr || opt.local_group != nullptr;
     c->rank = opt.rank;
     c->world = opt.world_size;
+    {
+      const char* pe = std::getenv("RHP_PEER_EXCHANGE");
+      const char* rep = std::getenv("RHP_DIST_REPLICATED");
+      c->sharded = c->dist && c->world > 1 && !(pe && pe[0] == '1') && !(rep && rep[0] == '1');
+    }
     if (c->dist) opt.use_graph = 0;  // NCCL calls are launched from the host loop
     c->opt = opt;
     if (lp->num_cons < 0 || lp->num_vars < 0 || lp->nnz < 0)
@@ -1112,9 +1261,16 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     c->n = L.n;
     cudaStream_t s = c->stream;
     const size_t m = static_cast<size_t>(c->m), n = static_cast<size_t>(c->n);
+    c->nalloc = c->n;
+    if (c->sharded) {
+      c->S = (c->n + c->world - 1) / c->world;
+      c->nlo = std::min<int64_t>(c->n, c->S * c->rank);
+      c->nhi = std::min<int64_t>(c->n, c->nlo + c->S);
+      c->nalloc = std::max<int64_t>(c->n, c->S * c->world);  // in-place all-gathers
+    }
     for (double** p2 : {&c->c, &c->vl, &c->vu, &c->co, &c->vlo, &c->vuo, &c->cs, &c->x, &c->aty,
                         &c->x0, &c->aty0, &c->xp, &c->xout, &c->rcout, &c->pv, &c->pw})
-      *p2 = dev_alloc<double>(n);
+      *p2 = dev_alloc<double>(static_cast<size_t>(c->nalloc));
     for (double** p2 : {&c->cl, &c->cu, &c->clo, &c->cuo, &c->rs, &c->y, &c->ax, &c->y0, &c->ax0,
                         &c->yp, &c->yout, &c->pav})
       *p2 = dev_alloc<double>(m);
@@ -1156,9 +1312,11 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     c->grid_vec = vec_grid(*c, std::max<int64_t>(c->m, c->n));
     // rank-independent n-side map (partitioned path): n and the device are
     // the same on every rank, so is this grid
-    c->grid_nside = vec_grid(*c, c->n);
+    // sharded: the walk covers the owned slice; S (not the slice length) sets
+    // the grid, so it is the same on every rank
+    c->grid_nside = vec_grid(*c, c->sharded ? c->S : c->n);
     c->nside.thread_rows = 1;
-    c->nside.rows = c->n;
+    c->nside.rows = c->sharded ? c->nhi - c->nlo : c->n;
     c->grid_max = std::max({c->grid_a, c->grid_at, c->grid_vec, c->grid_nside});
     for (double** p2 : {&c->part1, &c->part3, &c->partA, &c->partAt})
       *p2 = dev_alloc<double>(static_cast<size_t>(c->grid_max) * 16);
@@ -1183,7 +1341,12 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       CK(cudaMemsetAsync(p2, 0, std::max<size_t>(n, 1) * sizeof(double), s));
     for (double* p2 : {c->y, c->ax, c->y0, c->ax0, c->yp, c->yout, c->pav})
       CK(cudaMemsetAsync(p2, 0, std::max<size_t>(m, 1) * sizeof(double), s));
-    c->xchg = dev_alloc<double>(n + 16);
+    c->xchg = dev_alloc<double>(static_cast<size_t>(c->nalloc) + 16);  // zero tail: RS padding
+    if (c->sharded) {
+      c->rsb = dev_alloc<double>(static_cast<size_t>(c->S) + 8);
+      c->dsum = dev_alloc<double>(16);
+      c->ksum = dev_alloc<double>(16);
+    }
     CK(cudaStreamSynchronize(s));
     // small LPs: one cluster runs whole blocks when its CSR slices fit in
     // shared memory (auto) or when forced
@@ -1236,6 +1399,8 @@ int rhp_destroy(rhp_ctx* c) {
     if (p) cudaFree(p);
   if (c->agree) cudaFree(c->agree);
   if (c->opbuf) cudaFree(c->opbuf);
+  for (double* p : {c->rsb, c->dsum, c->ksum})
+    if (p) cudaFree(p);
   if (c->csc_src) cudaFree(c->csc_src);
   if (c->res_a_split) cudaFree(c->res_a_split);
   if (c->res_at_split) cudaFree(c->res_at_split);
@@ -1388,6 +1553,20 @@ int rhp_power_step(rhp_ctx* c, double* vw, double* ww) {
       e.w = c->pw;
       e.in[0] = c->pv;
       launch_spmv(*c, c->At, c->grid_at, c->pav, e, c->partAt, &c->ctl->ticket_pow, c->stream);
+    } else if (c->sharded) {  // owned slice of w = sum_p A_p^T (A_p v); dots allreduced
+      const int64_t lo = c->nlo;
+      launch_spmv(*c, c->At, c->grid_at, c->pav, store_into(c->xchg), nullptr, nullptr, c->stream);
+      c->comm->reduce_scatter(c->xchg, c->rsb, static_cast<size_t>(c->S), c->stream);
+      EpiPowerDist e{};
+      e.w = c->pw + lo;
+      e.in[0] = c->rsb;
+      e.in[1] = c->pv + lo;
+      epilogue_walk<EpiPowerDist><<<c->grid_nside, kBlock, 0, c->stream>>>(c->nside, e, c->partAt);
+      k_sum_partials<2><<<1, kBlock, 0, c->stream>>>(c->partAt, c->grid_nside, c->ksum);
+      CK(cudaGetLastError());
+      allreduce(*c, c->ksum, 2, c->stream);
+      k_power_from_sums<<<1, 32, 0, c->stream>>>(c->ctl, c->ksum);
+      CK(cudaGetLastError());
     } else {  // w = sum over ranks of A_p^T (A_p v), then v.w and w.w redundantly
       launch_spmv(*c, c->At, c->grid_at, c->pav, store_into(c->xchg), nullptr, nullptr,
                   c->stream);
@@ -1411,6 +1590,9 @@ int rhp_power_normalize(rhp_ctx* c, double wnorm) {
   return guarded([&] {
     k_normalize<<<c->grid_vec, kBlock, 0, c->stream>>>(c->pv, c->pw, wnorm, c->n);
     CK(cudaGetLastError());
+    // sharded: only the owned slice of w is current; every rank's slice of v
+    if (c->sharded)
+      c->comm->allgather(c->pv + c->nlo, c->pv, static_cast<size_t>(c->S) * sizeof(double), c->stream);
   });
 }
 
@@ -1597,6 +1779,11 @@ void gather_rows(rhp_ctx& c, const double* dev_local, double* host_full) {
 
 int rhp_fetch_solution(rhp_ctx* c, double* x, double* y, double* rcost) {
   return guarded([&] {
+    if (c->sharded) {  // the owners' slices of the unscaled x and reduced costs
+      const size_t b = static_cast<size_t>(c->S) * sizeof(double);
+      c->comm->allgather(c->xout + c->nlo, c->xout, b, c->stream);
+      c->comm->allgather(c->rcout + c->nlo, c->rcout, b, c->stream);
+    }
     if (x) download_perm(x, c->xout, c->L.pcol, c->hbuf, c->stream);
     if (y) {
       if (c->dist) gather_rows(*c, c->yout, y);
@@ -1631,6 +1818,11 @@ int rhp_any(rhp_ctx* c, int flag, int* any) {
 
 int rhp_fetch_iterate(rhp_ctx* c, double* x, double* y, double* ax, double* aty) {
   return guarded([&] {
+    if (c->sharded) {
+      const size_t b = static_cast<size_t>(c->S) * sizeof(double);
+      c->comm->allgather(c->x + c->nlo, c->x, b, c->stream);
+      c->comm->allgather(c->aty + c->nlo, c->aty, b, c->stream);
+    }
     const std::vector<int32_t> lrows = local_rows(*c);
     if (x) download_perm(x, c->x, c->L.pcol, c->hbuf, c->stream);
     if (y) download_perm(y, c->y, lrows, c->hbuf, c->stream);

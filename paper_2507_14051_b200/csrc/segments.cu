@@ -38,13 +38,18 @@ __device__ __forceinline__ int seg_of(const int32_t* cb, int S, int32_t c) {
   return lo;
 }
 
-// cnt[k * (rows + 1) + r] = elements of row r in segment k (zeroed before)
+// cnt[k * (rows + 1) + r] = elements of row r in segment k (zeroed before);
+// rows outside the band [rb, re) count everything in the last segment
 __global__ void k_seg_count(const int64_t* rp, const int32_t* ci, int64_t rows, const int32_t* cb,
-                            int S, int64_t* cnt) {
+                            int S, int64_t rb, int64_t re, int64_t* cnt) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
     const int64_t lo = rp[r], hi = rp[r + 1];
     if (lo == hi) continue;
+    if (r < rb || r >= re) {
+      cnt[static_cast<int64_t>(S - 1) * (rows + 1) + r] = hi - lo;
+      continue;
+    }
     int k = seg_of(cb, S, ci[lo]);
     int64_t run = 0;
     for (int64_t e = lo; e < hi; ++e) {
@@ -61,19 +66,22 @@ __global__ void k_seg_count(const int64_t* rp, const int32_t* ci, int64_t rows, 
 }
 
 __global__ void k_seg_scatter(const int64_t* rp, const int32_t* ci, const double* v, int64_t rows,
-                              const int32_t* cb, int S, int64_t* const* srp, int32_t* const* sci,
-                              double* const* sv) {
+                              const int32_t* cb, int S, int64_t rb, int64_t re,
+                              int64_t* const* srp, int32_t* const* sci, double* const* sv) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
     const int64_t lo = rp[r], hi = rp[r + 1];
     if (lo == hi) continue;
-    int k = seg_of(cb, S, ci[lo]);
-    int64_t out = srp[k][r];
+    const bool band = r >= rb && r < re;
+    // intermediate segments index the band's rows locally
+    auto start = [&](int k) { return k < S - 1 ? srp[k][r - rb] : srp[S - 1][r]; };
+    int k = band ? seg_of(cb, S, ci[lo]) : S - 1;
+    int64_t out = start(k);
     for (int64_t e = lo; e < hi; ++e) {
       const int32_t c = ci[e];
-      if (c >= cb[k + 1]) {
+      if (band && c >= cb[k + 1]) {
         k = seg_of(cb, S, c);
-        out = srp[k][r];
+        out = start(k);
       }
       sci[k][out] = c;
       sv[k][out] = v[e];
@@ -84,8 +92,9 @@ __global__ void k_seg_scatter(const int64_t* rp, const int32_t* ci, const double
 
 }  // namespace
 
-void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, std::vector<DeviceCsr>& out,
-                   std::vector<std::vector<int64_t>>& host_rp, cudaStream_t s) {
+void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, int64_t rb, int64_t re,
+                   std::vector<DeviceCsr>& out, std::vector<std::vector<int64_t>>& host_rp,
+                   cudaStream_t s) {
   const int S = static_cast<int>(cb.size()) - 1;
   const int64_t rows = op.rows;
   out.assign(static_cast<size_t>(S), DeviceCsr{});
@@ -93,7 +102,7 @@ void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, std::vec
   int32_t* d_cb = dev_alloc_zero<int32_t>(cb.size());
   int64_t* cnt = dev_alloc_zero<int64_t>(static_cast<size_t>(S) * (rows + 1));
   SCK(cudaMemcpyAsync(d_cb, cb.data(), cb.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  k_seg_count<<<blocks_for(rows), kThreads, 0, s>>>(op.rp, op.ci, rows, d_cb, S, cnt);
+  k_seg_count<<<blocks_for(rows), kThreads, 0, s>>>(op.rp, op.ci, rows, d_cb, S, rb, re, cnt);
   SCK(cudaGetLastError());
   size_t tb = 0;
   SCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, op.rp, rows + 1, s));
@@ -104,13 +113,16 @@ void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, std::vec
   std::vector<double*> pv(S);
   for (int k = 0; k < S; ++k) {
     DeviceCsr& d = out[k];
-    d.rows = rows;
-    d.rp = dev_alloc_zero<int64_t>(rows + 1);
-    SCK(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt + static_cast<int64_t>(k) * (rows + 1), d.rp, rows + 1, s));
-    host_rp[k].resize(static_cast<size_t>(rows) + 1);
-    SCK(cudaMemcpyAsync(host_rp[k].data(), d.rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    // intermediate segments: the band's rows only; the last one: all rows
+    const int64_t r0 = k < S - 1 ? rb : 0, nr = k < S - 1 ? re - rb : rows;
+    d.rows = nr;
+    d.rp = dev_alloc_zero<int64_t>(nr + 1);
+    SCK(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt + static_cast<int64_t>(k) * (rows + 1) + r0, d.rp,
+                                      nr + 1, s));
+    host_rp[k].resize(static_cast<size_t>(nr) + 1);
+    SCK(cudaMemcpyAsync(host_rp[k].data(), d.rp, (nr + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SCK(cudaStreamSynchronize(s));
-    d.nnz = host_rp[k][rows];
+    d.nnz = host_rp[k][nr];
     d.ci = dev_alloc_zero<int32_t>(d.nnz);
     d.v = dev_alloc_zero<double>(d.nnz);
     prp[k] = d.rp;
@@ -123,7 +135,8 @@ void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, std::vec
   SCK(cudaMemcpyAsync(d_prp, prp.data(), S * sizeof(int64_t*), cudaMemcpyHostToDevice, s));
   SCK(cudaMemcpyAsync(d_pci, pci.data(), S * sizeof(int32_t*), cudaMemcpyHostToDevice, s));
   SCK(cudaMemcpyAsync(d_pv, pv.data(), S * sizeof(double*), cudaMemcpyHostToDevice, s));
-  k_seg_scatter<<<blocks_for(rows), kThreads, 0, s>>>(op.rp, op.ci, op.v, rows, d_cb, S, d_prp, d_pci, d_pv);
+  k_seg_scatter<<<blocks_for(rows), kThreads, 0, s>>>(op.rp, op.ci, op.v, rows, d_cb, S, rb, re, d_prp,
+                                                      d_pci, d_pv);
   SCK(cudaGetLastError());
   SCK(cudaStreamSynchronize(s));
   for (void* p : {(void*)d_prp, (void*)d_pci, (void*)d_pv, (void*)d_cb, (void*)cnt, tmp}) cudaFree(p);

@@ -20,9 +20,15 @@
 namespace rhp {
 
 // Splits `op` (rows x cols, columns ascending inside every row) into
-// cb.size()-1 column segments [cb[k], cb[k+1]); out[k] gets its own row
+// S = cb.size()-1 column segments [cb[k], cb[k+1]); out[k] gets its own row
 // pointers, int32 columns and (current) values, host_rp[k] its row pointers.
-void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, std::vector<DeviceCsr>& out,
-                   std::vector<std::vector<int64_t>>& host_rp, cudaStream_t s);
+// Only the rows of the band [rb, re) are split: the intermediate segments
+// k < S-1 are CSRs over those rows alone (local row r - rb), and every row
+// outside the band keeps all its elements in the last segment (which spans
+// all rows). Rows whose gathers are already L2-local (C4's commodity-blocked
+// conservation and capacity rows) then cost one pass, not S.
+void split_columns(const DeviceCsr& op, const std::vector<int32_t>& cb, int64_t rb, int64_t re,
+                   std::vector<DeviceCsr>& out, std::vector<std::vector<int64_t>>& host_rp,
+                   cudaStream_t s);
 
 }  // namespace rhp

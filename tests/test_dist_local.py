@@ -10,6 +10,10 @@ non-zero row offsets, the distributed scaling, power iteration and KKT
 checks, gather_rows, the stop polling of partitioned plain blocks — runs
 here for real; only the transport differs from NCCL.
 
+Both exchanges of SURVEY.md §8(e) run: Option B (the default at world > 1:
+reduce-scatter of A^T y, n-side walk on the owned column slice, all-gather
+of x+) and Option A (RHP_DIST_REPLICATED=1: allreduce, replicated walk).
+
 Checks: every rank reports the same solve (bitwise); the first iterates
 equal the single-GPU path's within 1e-12 relative (the only difference is
 the summation order of A^T y across row blocks); solves match the single
@@ -72,9 +76,19 @@ def rel(a, b):
     return float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300))
 
 
+@pytest.fixture(params=["sharded", "replicated"])
+def exchange(request, monkeypatch):
+    """Option B (reduce-scatter + all-gather, n-side walk on the owned column
+    slice; the default at world > 1) or Option A (allreduce, replicated
+    n-side walk; RHP_DIST_REPLICATED=1)."""
+    if request.param == "replicated":
+        monkeypatch.setenv("RHP_DIST_REPLICATED", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("name", sorted(LPS))
 @pytest.mark.parametrize("world", [2, 3])
-def test_ranks_agree_and_match_single_gpu(gpu, name, world):
+def test_ranks_agree_and_match_single_gpu(gpu, name, world, exchange):
     lp = LPS[name]()
     off = partition_rows(lp, world)
     assert np.all(np.diff(off) > 0)  # every rank owns rows (non-zero row_begin)
@@ -97,7 +111,7 @@ def test_ranks_agree_and_match_single_gpu(gpu, name, world):
 
 
 @pytest.mark.parametrize("name", sorted(LPS))
-def test_first_iterates_match_single_gpu(gpu, name):
+def test_first_iterates_match_single_gpu(gpu, name, exchange):
     lp = LPS[name]()
     for k in (1, 10, 64, 65, 100):
         cfg = SolverConfig(epsilon=1e-300, iteration_limit=k)
@@ -108,7 +122,7 @@ def test_first_iterates_match_single_gpu(gpu, name):
         assert rel(got.y, want.y) <= 1e-12, (k, rel(got.y, want.y))
 
 
-def test_partitioned_with_column_segments(gpu, monkeypatch):
+def test_partitioned_with_column_segments(gpu, monkeypatch, exchange):
     """Forced 1 KB column segments on every rank's operators."""
     monkeypatch.setenv("RHP_SEG_BYTES", "1024")
     monkeypatch.setenv("RHP_SEG_FORCE", "1")
@@ -120,7 +134,7 @@ def test_partitioned_with_column_segments(gpu, monkeypatch):
     assert abs(got.objective - ref.objective) <= 1e-6 * max(1.0, abs(ref.objective))
 
 
-def test_iteration_limit_and_restart_stops_are_exact(gpu):
+def test_iteration_limit_and_restart_stops_are_exact(gpu, exchange):
     """Blocks that stop on the device mid-block (restart verdicts) and at the
     iteration limit: the stop polling issues no extra iteration (counts equal
     the single-GPU path's)."""
@@ -132,3 +146,17 @@ def test_iteration_limit_and_restart_stops_are_exact(gpu):
         assert [r.iterations for r in reps] == [limit, limit]
         assert reps[0].restart_count == ref.restart_count
         assert reps[0].kkt_checks == ref.kkt_checks
+
+
+def test_sharded_more_ranks_than_slices_of_work(gpu):
+    """World 4 on a tiny LP: uneven and empty column slices (n = 5)."""
+    from paper_2507_14051_b200 import LpProblem
+
+    lp = LpProblem(4, 5, [0, 2, 4, 6, 7], [0, 3, 1, 4, 0, 2, 3], [1.0, 2.0, -1.0, 1.0, 3.0, 1.0, 1.0],
+                   [1.0, -1.0, 2.0, 0.5, -0.5], [0.0] * 5, [4.0] * 5, [1.0, -1.0, 0.0, 0.5],
+                   [2.0, 1.0, 3.0, 0.5])
+    cfg = SolverConfig(epsilon=1e-8)
+    reps = solve_ranks(lp, cfg, 4)
+    ref = single(lp, cfg)
+    assert all(r.status == ref.status for r in reps)
+    assert abs(reps[0].objective - ref.objective) <= 1e-6 * max(1.0, abs(ref.objective))

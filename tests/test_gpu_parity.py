@@ -271,14 +271,18 @@ def test_spmv_engines_and_gather_policies(gpu, lp, monkeypatch):
 SEG_LPS = [c1_small(m=300, n=500), c3_transport(S=40, T=70)]
 
 
+@pytest.mark.parametrize("band", [None, (0.3, 0.7), (0.0, 0.25), (0.8, 1.0)],
+                         ids=["all_rows", "mid_band", "head_band", "tail_band"])
 @pytest.mark.parametrize("lp", SEG_LPS, ids=[c.name for c in SEG_LPS])
-def test_column_segments_match_oracle(gpu, lp, monkeypatch):
+def test_column_segments_match_oracle(gpu, lp, band, monkeypatch):
     """Column-segmented operators (built after scaling when the gathered
     vector exceeds RHP_SEG_BYTES; forced here with a 1 KB segment): SpMV
     within 1e-13 of the oracle, solves that match the reference (objective
     1e-6, KKT at eps, first iterates 1e-10) and stay deterministic."""
     monkeypatch.setenv("RHP_SEG_BYTES", "1024")
     monkeypatch.setenv("RHP_SEG_FORCE", "1")
+    if band is not None:  # only this row band (rows of A; A^T reads it as its own rows)
+        monkeypatch.setenv("RHP_SEG_BAND", f"{int(band[0] * lp.num_cons)},{int(band[1] * lp.num_cons)}")
     rng = np.random.default_rng(9)
     x = rng.uniform(-1, 1, lp.num_vars)
     y = rng.uniform(-1, 1, lp.num_cons)

@@ -5,7 +5,7 @@ forced column segments), the cluster-resident kernel's DSMEM reductions and
 barriers, the per-op API kernels (through the reference's own unit tests),
 and the peer-memory exchange's release/acquire flags (one rank). Each case
 runs in its own process (tools/sanitize_case.py) and must report
-"ERROR SUMMARY: 0 errors".
+zero errors (and, for racecheck, zero hazards).
 """
 import shutil
 import subprocess
@@ -26,7 +26,10 @@ CASES = [("resident", "memcheck"), ("resident", "racecheck"), ("resident", "sync
 def _run(cmd, timeout=900):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=str(ROOT))
     out = r.stdout + r.stderr
-    assert "ERROR SUMMARY: 0 errors" in out, out[-6000:]
+    # memcheck / synccheck end with "ERROR SUMMARY: 0 errors", racecheck with
+    # "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)"
+    assert ("ERROR SUMMARY: 0 errors" in out or
+            "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" in out), out[-6000:]
     assert r.returncode == 0, out[-6000:]
     return out
 

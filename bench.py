@@ -412,11 +412,16 @@ def run_product(args):
     # (column-segmented operators: one launch per segment; cluster-resident
     # small LPs: one launch per block)
     seg = layout.get("segments", {"A": 1, "At": 1})
-    per_it, per_chk = ((seg["A"] + seg["At"], seg["A"] + seg["At"]) if dist.world == 1
-                       else (seg["A"] + seg["At"] + 2, seg["A"] + seg["At"] + 2))
+    # partitioned: + control + n-side walk (sharded: + the x-side partial
+    # sum; KKT: + column walk + partial sum + from-sums); NCCL's own kernels
+    # are not counted
+    part = layout.get("partition", "single")
+    per_it = seg["A"] + seg["At"] + {"single": 0, "replicated": 2, "sharded": 3}[part]
+    per_chk = seg["A"] + seg["At"] + {"single": 0, "replicated": 2, "sharded": 3}[part]
+    blocks_extra = 1 if part == "sharded" else 0  # K3's partial sum
     if layout.get("resident"):
         per_it = 0
-    launches = per_it * iters + blocks + per_chk * checks
+    launches = per_it * iters + blocks * (1 + blocks_extra) + per_chk * checks
     t_max = dist.max(ms / 1e3)
     # one LP solved by all ranks together: the job's unit is a PDHG iteration
     value = iters / t_max
@@ -535,9 +540,15 @@ def run_product(args):
             "config": {"workload": WORKLOADS[args.config], "m": m, "n": n, "nnz": nnz,
                        "step": f"{STEP_ITERS} PDHG iterations + 1 KKT check (+ restarts)",
                        "parallelism": ("single GPU" if dist.world == 1 else
+                                       f"row-partitioned over {dist.world} GPUs: A x local; "
+                                       "per iteration the A^T y partials are NCCL "
+                                       "reduce-scattered to column-slice owners, 9 scalars "
+                                       "allreduced, the n-side update runs on the owned slice "
+                                       "and x+ is all-gathered (Option B)"
+                                       if part == "sharded" else
                                        f"row-partitioned over {dist.world} GPUs: A x local, "
-                                       "A^T y partials + scalars NCCL-allreduced per "
-                                       "iteration"),
+                                       "A^T y partials + scalars allreduced per iteration "
+                                       "(Option A)"),
                        "l2": "matrix (~24 B/nnz incl. A^T) larger than L2: no flush",
                        "layout": layout, "generation_s": gen_s,
                        "setup_s": info0["setup_seconds"]},

@@ -145,7 +145,8 @@ typedef struct rhp_layout_info {
                            bit 2: A uses the long-row (CTA row run) engine */
   int32_t segments;     /* column segments: A's in bits 0-15, A^T's in bits 16-31 (1 = unsegmented) */
   int32_t resident;     /* blocks run as one cluster-resident kernel (small LPs) */
-  int32_t pad_;
+  int32_t partition;    /* 0 single GPU, 1 row-partitioned with replicated n-side walk
+                           (Option A: allreduce / peer exchange), 2 sharded (Option B) */
 } rhp_layout_info;
 
 const char* rhp_last_error(void);

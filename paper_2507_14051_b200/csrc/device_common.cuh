@@ -135,7 +135,18 @@ constexpr int64_t kThreadRowMax = 8;
 // Operators whose every row has at least kCtaRowMin nonzeros use the long-row
 // engine (spmv.cuh spmv_cta_rows), kCtaRowsBatch rows per CTA pass.
 constexpr int64_t kCtaRowMin = 256;
-constexpr int kCtaRowsBatch = 8;
+#ifndef RHP_CTA_BATCH
+#define RHP_CTA_BATCH 2
+#endif
+#ifndef RHP_CTA_UNROLL
+#define RHP_CTA_UNROLL 4
+#endif
+#ifndef RHP_CTA_BLOCKS
+#define RHP_CTA_BLOCKS 4
+#endif
+constexpr int kCtaRowsBatch = RHP_CTA_BATCH;   // rows walked at once per CTA
+constexpr int kCtaRowUnroll = RHP_CTA_UNROLL;  // elements per row per thread in flight
+constexpr int kCtaRowBlocks = RHP_CTA_BLOCKS;  // resident CTAs per SM the kernel is built for
 #ifndef RHP_ROWS_IN_FLIGHT
 #define RHP_ROWS_IN_FLIGHT 2
 #endif

@@ -165,6 +165,7 @@ struct DevOp : DeviceCsr {
   double* segbuf = nullptr;  // [rows] running row sums of the segments
   // long-row engine (spmv_cta_rows): CTA b owns rows [cta_row[b], cta_row[b+1])
   int32_t* cta_row = nullptr;
+  int cta_grid = 0;  // its own grid (resident CTAs of spmv_cta_rows x SMs, at most one per row)
   // column segments: the row band [seg_rb, seg_re) split by columns; an
   // intermediate segment stores its band-local row sums at seg_out
   int64_t seg_rb = 0, seg_re = 0;
@@ -402,6 +403,7 @@ void launch_one(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const E
   cfg.numAttrs = c.pdl ? 1 : 0;
   if (op.cta_row) {
     const int32_t* cr = op.cta_row;
+    cfg.gridDim = dim3(static_cast<unsigned>(op.cta_grid));
     if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, true>, op.csr(), xg, op.sched, cr, epi, part, ticket));
     else CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, false>, op.csr(), xg, op.sched, cr, epi, part, ticket));
     return;
@@ -504,13 +506,21 @@ void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
 // balanced by nonzeros over the operator's grid. Only for A — A^T's
 // schedule is also walked by K3 / the partitioned walkers, which need the
 // merge-path or thread-per-row map. RHP_CTA_ROWS=0 disables it.
-void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp, int grid) {
+void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp) {
   const char* env = std::getenv("RHP_CTA_ROWS");
   if (env && env[0] == '0') return;
   const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
   if (rows < 1 || rows > INT32_MAX) return;
   for (int64_t r = 0; r < rows; ++r)
     if (rp[r + 1] - rp[r] < kCtaRowMin) return;
+  // as many CTAs as fit resident (all of them at once), at most one per row,
+  // never more than the partial buffers hold
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, reinterpret_cast<const void*>(spmv_cta_rows<EpiDual, false>), kBlock, 0));
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>({rows, static_cast<int64_t>(c.sm_count) * std::max(occ, 1),
+                            static_cast<int64_t>(c.grid_max)})));
   std::vector<int32_t> cr(static_cast<size_t>(grid) + 1, static_cast<int32_t>(rows));
   cr[0] = 0;
   const double total = static_cast<double>(rp[rows]);
@@ -521,6 +531,7 @@ void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp, int gr
     cr[b] = static_cast<int32_t>(r);
   }
   d.cta_row = dev_alloc<int32_t>(cr.size());
+  d.cta_grid = grid;
   upload(d.cta_row, cr.data(), cr.size(), c.stream);
   CK(cudaStreamSynchronize(c.stream));
   d.sched.thread_rows = 0;
@@ -530,7 +541,7 @@ void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp, int gr
 void choose_engines(rhp_ctx& c) {
   apply_engine_rule(c.A, c.L.A.rp);
   apply_engine_rule(c.At, c.L.At.rp);
-  apply_cta_rule(c, c.A, c.L.A.rp, c.grid_a);
+  apply_cta_rule(c, c.A, c.L.A.rp);
 }
 
 __global__ void k_mark_sectors(const int32_t* ci, int64_t lo, int64_t hi, unsigned int* bits) {
@@ -1055,7 +1066,7 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
   ec.xout = write_out ? c.xout : nullptr;
   ec.rcout = write_out ? c.rcout : nullptr;
   ec.part_row = c.partA;
-  ec.grid_row = c.grid_a;
+  ec.grid_row = c.A.cta_row ? c.A.cta_grid : c.grid_a;  // the A-side kernel's grid
   ec.n_multi_row = fin(c.A).sched.n_multi;
   ec.long_red_row = fin(c.A).long_red;
   if (!c.dist) {
@@ -1437,6 +1448,7 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0) |
                         (c->A.cta_row ? 4 : 0);
     info->resident = c->resident ? 1 : 0;
+    info->partition = !c->dist ? 0 : c->sharded ? 2 : 1;
     info->segments = static_cast<int32_t>(std::max<size_t>(1, c->A.segs.size()) |
                                           (std::max<size_t>(1, c->At.segs.size()) << 16));
   });

@@ -384,25 +384,28 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
 }
 
 // Long-row engine (an operator made of few very long rows, e.g. C3's A:
-// 2000 rows of 1000 nonzeros; rhp_cuda.cu apply_engine_rule, every row
-// >= kCtaRowMin nonzeros). CTA b owns the contiguous rows [cta_row[b],
-// cta_row[b+1]) (balanced by nonzeros on the host) and walks them kCtaRowsBatch
-// at a time: thread t takes elements t, t + kBlock, ... of every row of the
-// batch (coalesced index / value loads, kCtaRowsBatch independent gather
-// chains per thread), then each row's partials are reduced by a fixed
-// shuffle tree per warp and a fixed warp order in shared memory, and lane q
-// of warp 0 runs row q's epilogue. No split rows, no tickets, no slots: the
-// operator's n_multi is 0, so the finalize reads only the CTA partials.
-// Deterministic (fixed element -> thread map and reduction order).
+// 2000 rows of 1000 nonzeros; rhp_cuda.cu apply_cta_rule, every row >=
+// kCtaRowMin nonzeros). CTA b owns the contiguous rows [cta_row[b],
+// cta_row[b+1]) (balanced by nonzeros on the host) and walks them
+// kCtaRowsBatch at a time: thread t takes elements t, t + kBlock, ... of
+// every row of the batch, kCtaRowUnroll of them per row at once (coalesced
+// index / value loads, then all the batch's gathers in flight), then each
+// row's partials are reduced by a fixed shuffle tree per warp and a fixed
+// warp order in shared memory, and lane q of warp 0 runs row q's epilogue.
+// Built for kCtaRowBlocks CTAs per SM (register budget 64 at 256 threads) on
+// its own grid (DevOp::cta_grid): latency is hidden by resident warps rather
+// than by the long windows of the merge-path engine. No split rows, no
+// tickets, no slots (n_multi 0). Deterministic: fixed element -> thread map
+// and reduction order.
 template <class Epi, bool L1G = false>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_cta_rows(Csr A, const double* __restrict__ xg,
-                                                                    Sched s, const int32_t* cta_row,
-                                                                    Epi epi, double* part,
-                                                                    unsigned int* ticket) {
+__global__ void __launch_bounds__(kBlock, kCtaRowBlocks) spmv_cta_rows(Csr A, const double* __restrict__ xg,
+                                                                       Sched s, const int32_t* cta_row,
+                                                                       Epi epi, double* part,
+                                                                       unsigned int* ticket) {
   pdl_wait();
   pdl_trigger();
   if (!epi.enter()) return;
-  constexpr int RB = kCtaRowsBatch;
+  constexpr int RB = kCtaRowsBatch, K = kCtaRowUnroll;
   __shared__ double red[RB][kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[Epi::NRED];
@@ -421,18 +424,24 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_cta_rows(Csr A, const
       len = max(len, hi[q] - lo[q]);
       p[q] = 0.0;
     }
-    for (int64_t t = threadIdx.x; t < len; t += kBlock) {
-      int c[RB];
-      double v[RB];
-#pragma unroll
-      for (int q = 0; q < RB; ++q) {
-        const bool ok = lo[q] + t < hi[q];
-        c[q] = ok ? __ldcs(A.ci + lo[q] + t) : 0;
-        v[q] = ok ? __ldcs(A.v + lo[q] + t) : 0.0;
-      }
+    for (int64_t t0 = threadIdx.x; t0 < len; t0 += static_cast<int64_t>(K) * kBlock) {
+      int c[RB][K];
+      double v[RB][K];
 #pragma unroll
       for (int q = 0; q < RB; ++q)
-        if (lo[q] + t < hi[q]) p[q] = fma(v[q], ld_gather<L1G>(xg + c[q]), p[q]);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int64_t e = lo[q] + t0 + static_cast<int64_t>(k) * kBlock;
+          const bool ok = e < hi[q];
+          c[q][k] = ok ? __ldcs(A.ci + e) : 0;
+          v[q][k] = ok ? __ldcs(A.v + e) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < RB; ++q)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (lo[q] + t0 + static_cast<int64_t>(k) * kBlock < hi[q])
+            p[q] = fma(v[q][k], ld_gather<L1G>(xg + c[q][k]), p[q]);
     }
 #pragma unroll
     for (int q = 0; q < RB; ++q) {

@@ -299,6 +299,7 @@ int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
     o[25] = li.thread_rows;
     o[26] = li.segments;
     o[27] = li.resident;
+    o[28] = li.partition;
   });
 }
 

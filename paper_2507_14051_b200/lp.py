@@ -504,7 +504,7 @@ class Session:
         return {"A": ms[0], "At": ms[1]}
 
     def layout(self) -> dict:
-        o = (C.c_int64 * 28)()
+        o = (C.c_int64 * 29)()
         self._check(self._lib.rhpdhg_session_layout(self._h, o))
         return {"m": o[0], "n": o[1], "nnz": o[2], "row_bins": list(o[3:11]),
                 "col_bins": list(o[11:19]), "grid_a": o[19], "grid_at": o[20],
@@ -513,7 +513,8 @@ class Session:
                 "thread_rows": {"A": bool(o[25] & 1), "At": bool(o[25] & 2)},
                 "cta_rows": {"A": bool(o[25] & 4)},
                 "segments": {"A": int(o[26] & 0xffff), "At": int(o[26] >> 16)},
-                "resident": bool(o[27])}
+                "resident": bool(o[27]),
+                "partition": {0: "single", 1: "replicated", 2: "sharded"}[int(o[28])]}
 
     def finish(self) -> SolutionReport:
         def fn(view, cc, rep, x, y, rc_, hist, cap):

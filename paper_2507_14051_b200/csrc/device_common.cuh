@@ -62,42 +62,21 @@ __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p);
 __device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
 __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs((const long long*)p); }
 
-// Gather of the SpMV input vector. Default: L1::no_allocate — a random
-// gather over a vector much larger than L1 almost never hits, and allocating
-// evicts useful lines. L1G (RHP_L1_GATHER=1, rhp_cuda.cu
-// choose_gather_policy): the read-only L1-allocating path.
-#ifndef RHP_GATHER_MODE
-#define RHP_GATHER_MODE 2
-#endif
-// The gathered vector's L2 lines are marked evict_last (createpolicy +
-// L2::cache_hint), so the streamed matrix (evict_first) and the epilogue
-// vectors never push them out: C4 (x = 160 MB > L2) 1117 -> 1170 iter/s,
-// C2 +0.7 %, C3 and C5 neutral. RHP_GATHER_EVICT_LAST=0 restores the default
-// L2 policy.
-#ifndef RHP_GATHER_EVICT_LAST
-#define RHP_GATHER_EVICT_LAST 1
-#endif
+// Gather of the SpMV input vector: L1::no_allocate (a random gather over a
+// vector much larger than L1 almost never hits, and allocating evicts useful
+// lines) with an evict_last L2 policy (createpolicy + L2::cache_hint), so the
+// streamed matrix (evict_first) and the epilogue vectors never push the
+// gathered vector out of L2: C4 (x = 160 MB > L2) 1117 -> 1170 iter/s, C2
+// +0.7 %, C3 and C5 neutral. L1G (RHP_L1_GATHER=1, rhp_cuda.cu
+// choose_gather_policy): the L1-allocating variant of the same load.
 template <bool L1G = false>
 __device__ __forceinline__ double ld_gather(const double* p) {
-#if RHP_GATHER_EVICT_LAST
   double e;
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   if constexpr (L1G) asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(e) : "l"(p), "l"(pol));
   else asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(e) : "l"(p), "l"(pol));
   return e;
-#else
-  if constexpr (L1G) return __ldg(p);  // L1-allocating: small or clustered vectors
-#if RHP_GATHER_MODE == 1
-  return __ldcg(p);  // L2 only
-#elif RHP_GATHER_MODE == 2
-  double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);  // read-only path
-#endif
-#endif
 }
 
 // Programmatic dependent launch (launch_spmv sets the attribute): wait until
@@ -110,10 +89,11 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Bulk L2 prefetch (address and size multiples of 16 B; no completion).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
+// Merge-path engine: load a window's epilogue inputs (rows r .. r+31) before
+// its gathers (spmv.cuh chunk_range). Off by default (A/B variant).
+#ifndef RHP_EPI_PREFETCH
+#define RHP_EPI_PREFETCH 0
+#endif
 
 // 32-bit row / nonzero positions inside the SpMV warp walk.
 #ifndef RHP_IDX32

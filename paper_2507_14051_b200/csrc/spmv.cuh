@@ -147,6 +147,14 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
     const ix we = wb + kWin < e_end ? wb + kWin : e_end;  // valid end of the window
     // ends of the next 32 rows: group 0 of the flags and of the completion pass
     ix re0 = r + lane < r_lim ? static_cast<ix>(rp[r + lane + 1]) : kIxMax;
+#if RHP_EPI_PREFETCH
+    // epilogue inputs of row r + lane, loaded before the gathers: the first
+    // completion group below finishes exactly these rows (lane j <-> row
+    // r + j), so their loads leave the window's critical path
+    double epre[Epi::NIN > 0 ? Epi::NIN : 1];
+    const ix pre_row = r + lane;
+    if (pre_row < r_end) load_inputs(epi, pre_row, epre);
+#endif
     if constexpr (!WALK) {
       const ix mine = wb + kPer * lane;  // first element of this lane
       // (1) values and gathers of this window, then the next window's indices
@@ -155,11 +163,7 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
 #pragma unroll
       for (int t = 0; t < kPer; ++t) {
         const bool ok = mine + t >= e0 && mine + t < we;
-#ifdef RHP_FAKE_GATHER  // timing experiment only: gathers confined to 32 KB of x (L1 hits)
-        p[t] = ok ? ld_gather<L1G>(xg + (cn[t] & 0xfff)) : 0.0;
-#else
         p[t] = ok ? ld_gather<L1G>(xg + cn[t]) : 0.0;
-#endif
         if (!ok) vc[t] = 0.0;
       }
       if (mine + kWin < e_end) ld_idx(ci, mine + kWin, cn);
@@ -240,8 +244,17 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
           if constexpr (!WALK) {
             if (s.seg_in) sum = add(__ldcg(s.seg_in + row), sum);
           }
+#if RHP_EPI_PREFETCH
+          if (row == pre_row) {
+            epi.row(row, sum, epre, 1, acc);
+          } else {
+            load_inputs(epi, row, ein);
+            epi.row(row, sum, ein, 1, acc);
+          }
+#else
           load_inputs(epi, row, ein);
           epi.row(row, sum, ein, 1, acc);
+#endif
         }
       }
       const int nc = __popc(__ballot_sync(0xffffffffu, done));

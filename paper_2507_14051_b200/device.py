@@ -18,11 +18,11 @@ def _p(a):
 
 class DeviceContext:
     def __init__(self, lp: LpProblem, device: int = 0, use_graph: bool = True,
-                 block_limit: int = 64):
+                 block_limit: int = 64, resident: int = 0):
         self.lib = capi.load_cuda()
         self.lp = lp
         opt = capi.RhpOptions(device=device, rank=0, world_size=1, use_graph=int(use_graph),
-                              block_limit=block_limit, nccl_id=None)
+                              block_limit=block_limit, nccl_id=None, resident=resident)
         h = C.c_void_p()
         self._view = lp.view()
         self._ok(self.lib.rhp_create(C.byref(self._view), C.byref(opt), C.byref(h)))

@@ -376,3 +376,41 @@ def test_invalid_inputs_raise_reference_errors(gpu):
     ok = LpProblem(1, 1, [0, 1], [0], [1.0], [1.0], [0.0], [1.0], [0.0], [1.0])
     with pytest.raises(UsageError):
         solve(ok, SolverConfig(stepsize_multiplier=1.5))
+
+
+@pytest.mark.parametrize("resident,graph", [(0, True), (0, False), (1, True)],
+                         ids=["graph", "plain", "resident"])
+def test_device_breakdown_branch(gpu, resident, graph):
+    """The indefinite-norm branch of the device control (pdhg.cpp:101-115):
+    a step that violates eta ||A|| <= 1 (a = 2, eta = 1, set directly on the
+    device: solve() would reject it with UsageError) drives the fixed-point
+    radicand below both roundoff floors in the second iteration, q = -18
+    exactly (hand value of the reference formulas on this 1x1 LP); the block
+    stops there with the breakdown flag, in every engine and launch mode."""
+    from paper_2507_14051_b200 import LpProblem
+
+    lp = LpProblem(1, 1, [0, 1], [0], [2.0], [1.0], [-10.0], [10.0], [1.0], [1.0])
+    with DeviceContext(lp, use_graph=graph, resident=resident) as dev:
+        dev.scale(enabled=False)
+        eta = 1.0
+        dev.set_step(eta=eta, omega=1.0, gamma=1.0, tau=eta, sigma=eta, sigma_inv=1.0 / eta,
+                     primal_scale=1.0 / eta, dual_scale=1.0 / eta, beta_sufficient=0.2,
+                     beta_necessary=0.8, beta_artificial=0.36, check_interval=64,
+                     iteration_limit=1000, restarts_enabled=0, record_history=0)
+        dev.reset_iterate()
+        out = dev.run_block()
+    assert out["breakdown"] == 1
+    assert out["iterations_done"] == 2 and out["q_last"] == -18.0
+
+
+def test_device_kkt_counts_nan_iterates(gpu):
+    """A NaN iterate is counted by the device KKT sums (the host turns the
+    count into NumericalBreakdownError, termination.cpp:58-118)."""
+    from paper_2507_14051_b200 import LpProblem, NumericalBreakdownError
+
+    lp = LpProblem(1, 1, [0, 1], [0], [2.0], [1.0], [-10.0], [10.0], [1.0], [1.0])
+    with DeviceContext(lp, use_graph=False) as dev:
+        dev.scale(enabled=False)
+        dev.set_iterate([float("nan")], [0.0])
+        s = dev.kkt(0)
+    assert s["nan_x"] == 1

@@ -147,14 +147,18 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
     const ix we = wb + kWin < e_end ? wb + kWin : e_end;  // valid end of the window
     // ends of the next 32 rows: group 0 of the flags and of the completion pass
     ix re0 = r + lane < r_lim ? static_cast<ix>(rp[r + lane + 1]) : kIxMax;
-#if RHP_EPI_PREFETCH
-    // epilogue inputs of row r + lane, loaded before the gathers: the first
-    // completion group below finishes exactly these rows (lane j <-> row
-    // r + j), so their loads leave the window's critical path
+    // epilogue inputs of row r + lane, loaded at the top of the window: the
+    // first completion group below finishes exactly these rows (lane j <->
+    // row r + j), so their loads leave the window's critical path. Used by
+    // the walkers (K3: 21 -> 15 us on C2); in the SpMV proper the extra live
+    // registers cost more than they hide (C2 K1 68.8 -> 71.9 us, C4 K1
+    // 674 -> 698 us), so there only with RHP_EPI_PREFETCH=1.
+    constexpr bool kPre = WALK || RHP_EPI_PREFETCH;
     double epre[Epi::NIN > 0 ? Epi::NIN : 1];
     const ix pre_row = r + lane;
-    if (pre_row < r_end) load_inputs(epi, pre_row, epre);
-#endif
+    if constexpr (kPre) {
+      if (pre_row < r_end) load_inputs(epi, pre_row, epre);
+    }
     if constexpr (!WALK) {
       const ix mine = wb + kPer * lane;  // first element of this lane
       // (1) values and gathers of this window, then the next window's indices
@@ -244,17 +248,12 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
           if constexpr (!WALK) {
             if (s.seg_in) sum = add(__ldcg(s.seg_in + row), sum);
           }
-#if RHP_EPI_PREFETCH
-          if (row == pre_row) {
+          if (kPre && row == pre_row) {
             epi.row(row, sum, epre, 1, acc);
           } else {
             load_inputs(epi, row, ein);
             epi.row(row, sum, ein, 1, acc);
           }
-#else
-          load_inputs(epi, row, ein);
-          epi.row(row, sum, ein, 1, acc);
-#endif
         }
       }
       const int nc = __popc(__ballot_sync(0xffffffffu, done));

@@ -408,6 +408,17 @@ void launch_one(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const E
     else CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, false>, op.csr(), xg, op.sched, cr, epi, part, ticket));
     return;
   }
+#if RHP_STAGE
+  cfg.dynamicSmemBytes = static_cast<size_t>(kStageBytes) * kWarps;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(spmv_fused<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(cfg.dynamicSmemBytes)));
+    CK(cudaFuncSetAttribute(spmv_fused<Epi, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(cfg.dynamicSmemBytes)));
+    attr_set = true;
+  }
+#endif
   if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
   else CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
 }
@@ -437,10 +448,18 @@ void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const 
 template <class Epi>
 int prepare_spmv() {
   int b = 0, b1 = 0;
+  size_t dyn = 0;
+#if RHP_STAGE
+  dyn = static_cast<size_t>(kStageBytes) * kWarps;
+  CK(cudaFuncSetAttribute(spmv_fused<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(dyn)));
+  CK(cudaFuncSetAttribute(spmv_fused<Epi, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(dyn)));
+#endif
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &b, reinterpret_cast<const void*>(spmv_fused<Epi, false>), kBlock, 0));
+      &b, reinterpret_cast<const void*>(spmv_fused<Epi, false>), kBlock, dyn));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &b1, reinterpret_cast<const void*>(spmv_fused<Epi, true>), kBlock, 0));
+      &b1, reinterpret_cast<const void*>(spmv_fused<Epi, true>), kBlock, dyn));
   b = std::min(b, b1);
   if (b < 1) throw CudaError("spmv kernel does not fit on an SM");
   return b;
@@ -841,7 +860,7 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
 void sharded_walk_tail(rhp_ctx& c, cudaStream_t s) {
   k_sum_partials<4><<<1, kBlock, 0, s>>>(c.part3, c.grid_nside, c.dsum + 5);
   CK(cudaGetLastError());
-  c.comm->allgather(c.xp + c.nlo, c.xp, static_cast<size_t>(c.S) * sizeof(double), s);
+  c.comm->allgather(c.xp + c.S * c.rank, c.xp, static_cast<size_t>(c.S) * sizeof(double), s);
 }
 
 // One iteration of the sharded partitioned path (Option B, rhp_ctx::sharded).
@@ -1077,7 +1096,8 @@ void run_kkt(rhp_ctx& c, const double* xs, const double* ys, bool refresh, bool 
     // (4..9) sums meet in one 10-scalar allreduce
     cudaStream_t s = c.stream;
     const int64_t lo = c.nlo;
-    if (xs == c.x) c.comm->allgather(c.x + lo, c.x, static_cast<size_t>(c.S) * sizeof(double), s);
+    if (xs == c.x)
+      c.comm->allgather(c.x + c.S * c.rank, c.x, static_cast<size_t>(c.S) * sizeof(double), s);
     EpiKktRowDist rd{};
     static_cast<EpiKktRow&>(rd) = er;
     rd.xsums = c.ksum;
@@ -1604,7 +1624,8 @@ int rhp_power_normalize(rhp_ctx* c, double wnorm) {
     CK(cudaGetLastError());
     // sharded: only the owned slice of w is current; every rank's slice of v
     if (c->sharded)
-      c->comm->allgather(c->pv + c->nlo, c->pv, static_cast<size_t>(c->S) * sizeof(double), c->stream);
+      c->comm->allgather(c->pv + c->S * c->rank, c->pv, static_cast<size_t>(c->S) * sizeof(double),
+                         c->stream);
   });
 }
 
@@ -1793,8 +1814,8 @@ int rhp_fetch_solution(rhp_ctx* c, double* x, double* y, double* rcost) {
   return guarded([&] {
     if (c->sharded) {  // the owners' slices of the unscaled x and reduced costs
       const size_t b = static_cast<size_t>(c->S) * sizeof(double);
-      c->comm->allgather(c->xout + c->nlo, c->xout, b, c->stream);
-      c->comm->allgather(c->rcout + c->nlo, c->rcout, b, c->stream);
+      c->comm->allgather(c->xout + c->S * c->rank, c->xout, b, c->stream);
+      c->comm->allgather(c->rcout + c->S * c->rank, c->rcout, b, c->stream);
     }
     if (x) download_perm(x, c->xout, c->L.pcol, c->hbuf, c->stream);
     if (y) {
@@ -1832,8 +1853,8 @@ int rhp_fetch_iterate(rhp_ctx* c, double* x, double* y, double* ax, double* aty)
   return guarded([&] {
     if (c->sharded) {
       const size_t b = static_cast<size_t>(c->S) * sizeof(double);
-      c->comm->allgather(c->x + c->nlo, c->x, b, c->stream);
-      c->comm->allgather(c->aty + c->nlo, c->aty, b, c->stream);
+      c->comm->allgather(c->x + c->S * c->rank, c->x, b, c->stream);
+      c->comm->allgather(c->aty + c->S * c->rank, c->aty, b, c->stream);
     }
     const std::vector<int32_t> lrows = local_rows(*c);
     if (x) download_perm(x, c->x, c->L.pcol, c->hbuf, c->stream);

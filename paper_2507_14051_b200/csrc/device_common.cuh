@@ -79,36 +79,6 @@ __device__ __forceinline__ double ld_gather(const double* p) {
   return e;
 }
 
-// ---- bulk async copies (TMA engine, 1-D) into shared memory with mbarrier
-// completion: the staged merge-path windows (RHP_STAGE, spmv.cuh).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* mb, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(mb))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
-          smem_u32(mb)),
-      "r"(parity)
-      : "memory");
-}
-
 // Programmatic dependent launch (launch_spmv sets the attribute): wait until
 // the preceding kernel has completed and its writes are visible (a no-op when
 // launched without the attribute), then let the next kernel's CTAs be
@@ -118,13 +88,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-
-// Merge-path engine, experimental: each warp's window indices and values
-// arrive by 1-D bulk async copies (TMA) into a 2-deep shared-memory ring,
-// prefetched two windows ahead, instead of register-held vector loads.
-#ifndef RHP_STAGE
-#define RHP_STAGE 0
-#endif
 
 // Merge-path engine: load a window's epilogue inputs (rows r .. r+31) before
 // its gathers (spmv.cuh chunk_range). Off by default (A/B variant).

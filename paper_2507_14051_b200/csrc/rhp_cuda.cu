@@ -408,17 +408,6 @@ void launch_one(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const E
     else CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, false>, op.csr(), xg, op.sched, cr, epi, part, ticket));
     return;
   }
-#if RHP_STAGE
-  cfg.dynamicSmemBytes = static_cast<size_t>(kStageBytes) * kWarps;
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(spmv_fused<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(cfg.dynamicSmemBytes)));
-    CK(cudaFuncSetAttribute(spmv_fused<Epi, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(cfg.dynamicSmemBytes)));
-    attr_set = true;
-  }
-#endif
   if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
   else CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
 }
@@ -448,14 +437,7 @@ void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const 
 template <class Epi>
 int prepare_spmv() {
   int b = 0, b1 = 0;
-  size_t dyn = 0;
-#if RHP_STAGE
-  dyn = static_cast<size_t>(kStageBytes) * kWarps;
-  CK(cudaFuncSetAttribute(spmv_fused<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(dyn)));
-  CK(cudaFuncSetAttribute(spmv_fused<Epi, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(dyn)));
-#endif
+  const size_t dyn = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &b, reinterpret_cast<const void*>(spmv_fused<Epi, false>), kBlock, dyn));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(

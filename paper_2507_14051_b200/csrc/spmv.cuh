@@ -61,19 +61,6 @@ struct WarpSmem {
   unsigned char flag[kWin];  // 1 where a row starts
 };
 
-// RHP_STAGE: one warp's 2-deep ring of window copies (dynamic shared memory,
-// kStageBytes per warp) and its mbarrier phase bits.
-struct WarpStage {
-  int32_t idx[2][kWin];
-  double val[2][kWin];
-  uint64_t mb[2];
-};
-constexpr int kStageBytes = static_cast<int>(sizeof(WarpStage));
-struct StageState {
-  WarpStage* st = nullptr;
-  uint32_t ph0 = 0, ph1 = 0;
-};
-
 // Column indices / values of the kPer nonzeros of one lane starting at
 // element i (a multiple of 4). Reads at most 3 elements past the operator's
 // end (inside the 64-B padding of every device array).
@@ -136,8 +123,7 @@ __device__ __forceinline__ void contribute(const Sched& s, Epi& epi, int slot, i
 template <class Epi, bool WALK, bool L1G = false>
 __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, const double* vals,
                                             const double* __restrict__ xg, const Sched& s,
-                                            Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm,
-                                            StageState& ss) {
+                                            Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
   const int lane = threadIdx.x & 31;
   // row and nonzero positions fit 32 bits (ingest.cu caps an operator at
   // 2^31 - 2^16 nonzeros): 32-bit locals halve their registers and shuffles
@@ -154,29 +140,9 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
   // [e0, e_end) are masked to zero
   ix wb = e0 & ~ix(3);
   int cn[kPer];  // column indices of this lane's elements of the current window
-#if RHP_STAGE
-  // window copies into the ring: buffer b of window i is i & 1; issued two
-  // windows ahead by lane 0, only for windows inside this chunk
-  const ix e_end4 = (e_end + 3) & ~ix(3);
-  auto issue = [&](ix wstart, int b) {
-    if (wstart >= e_end) return;
-    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<ix>(kWin), e_end4 - wstart));
-    mbar_expect_tx(&ss.st->mb[b], cnt * 12u);
-    bulk_g2s(ss.st->idx[b], ci + wstart, cnt * 4u, &ss.st->mb[b]);
-    bulk_g2s(ss.st->val[b], vals + wstart, cnt * 8u, &ss.st->mb[b]);
-  };
-  int buf = 0;
-  if constexpr (!WALK) {
-    if (lane == 0) {
-      issue(wb, 0);
-      issue(wb + kWin, 1);
-    }
-  }
-#else
   if constexpr (!WALK) {
     if (wb + kPer * lane < e_end) ld_idx(ci, wb + kPer * lane, cn);
   }
-#endif
   for (;; wb += kWin) {
     const ix we = wb + kWin < e_end ? wb + kWin : e_end;  // valid end of the window
     // ends of the next 32 rows: group 0 of the flags and of the completion pass
@@ -197,44 +163,14 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
       const ix mine = wb + kPer * lane;  // first element of this lane
       // (1) values and gathers of this window, then the next window's indices
       double p[kPer], vc[kPer];
-#if RHP_STAGE
-      {
-        const uint32_t par = buf ? ss.ph1 : ss.ph0;
-        mbar_wait(&ss.st->mb[buf], par);
-        if (buf) ss.ph1 ^= 1u;
-        else ss.ph0 ^= 1u;
-        const int o = kPer * lane;
-#pragma unroll
-        for (int h = 0; h < kPer / 4; ++h) {
-          const int4 q = *reinterpret_cast<const int4*>(&ss.st->idx[buf][o + 4 * h]);
-          cn[4 * h + 0] = q.x;
-          cn[4 * h + 1] = q.y;
-          cn[4 * h + 2] = q.z;
-          cn[4 * h + 3] = q.w;
-        }
-#pragma unroll
-        for (int h = 0; h < kPer / 2; ++h) {
-          const double2 d = *reinterpret_cast<const double2*>(&ss.st->val[buf][o + 2 * h]);
-          vc[2 * h + 0] = d.x;
-          vc[2 * h + 1] = d.y;
-        }
-      }
-#else
       if (mine < we) ld_vals(vals, mine, vc);
-#endif
 #pragma unroll
       for (int t = 0; t < kPer; ++t) {
         const bool ok = mine + t >= e0 && mine + t < we;
         p[t] = ok ? ld_gather<L1G>(xg + cn[t]) : 0.0;
         if (!ok) vc[t] = 0.0;
       }
-#if RHP_STAGE
-      __syncwarp();  // every lane has read ring buffer `buf`: refill it
-      if (lane == 0) issue(wb + 2 * kWin, buf);
-      buf ^= 1;
-#else
       if (mine + kWin < e_end) ld_idx(ci, mine + kWin, cn);
-#endif
       // (2) row-start flags
 #pragma unroll
       for (int h = 0; h < kPer / 4; ++h) reinterpret_cast<uint32_t*>(sm.flag)[lane * (kPer / 4) + h] = 0u;
@@ -350,23 +286,10 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
 template <class Epi, bool WALK, bool L1G = false>
 __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals,
                                            const double* __restrict__ xg, const Sched& s,
-                                           Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm,
-                                           WarpStage* stage = nullptr) {
+                                           Epi& epi, double (&acc)[Epi::NRED], WarpSmem& sm) {
   const int w = static_cast<int>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
-  StageState ss;
-  ss.st = stage;
-#if RHP_STAGE
-  if constexpr (!WALK) {
-    if ((threadIdx.x & 31) == 0) {
-      mbar_init(&stage->mb[0], 1);
-      mbar_init(&stage->mb[1], 1);
-      mbar_fence_init();
-    }
-    __syncwarp();
-  }
-#endif
   for (int c = w; c < s.n_chunks; c += s.n_warps)
-    chunk_range<Epi, WALK, L1G>(c, ci, vals, xg, s, epi, acc, sm, ss);
+    chunk_range<Epi, WALK, L1G>(c, ci, vals, xg, s, epi, acc, sm);
 }
 
 // Thread-per-row engine, for operators whose rows are all short
@@ -459,17 +382,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  if (s.thread_rows) {
-    thread_rows<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc);
-  } else {
-#if RHP_STAGE
-    extern __shared__ __align__(128) unsigned char stage_raw[];
-    WarpStage* stage = reinterpret_cast<WarpStage*>(stage_raw) + (threadIdx.x >> 5);
-    warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5], stage);
-#else
-    warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
-#endif
-  }
+  if (s.thread_rows) thread_rows<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc);
+  else warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
   if constexpr (Epi::REDUCE) {
     block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
     if constexpr (Epi::FINAL) {

@@ -268,12 +268,6 @@ struct rhp_ctx {
 
 namespace {
 
-int occupancy_blocks(const void* fn) {
-  int b = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kBlock, 0));
-  return std::max(b, 1);
-}
-
 // Uploads the warp schedule of an operator (built for the operator's grid).
 void upload_sched(DevOp& d, const HostOperator& h, cudaStream_t s) {
   const size_t W = static_cast<size_t>(h.sched.n_chunks), ns = h.slot_row.size();

@@ -322,6 +322,36 @@ def generators_nnz_c5():
     return 50_000_000 * 20
 
 
+def cpu_baseline_leg(args, lp, e2e):
+    """The reference on this LP (C5: on a 1/50-scale instance of its
+    generator, extrapolated linearly in nnz), with the time-to-tolerance
+    extrapolated from the GPU's iteration count."""
+    if args.config == "c5":
+        small = generators.c5_rowpart(**C5_CPU_SAMPLE)
+        n_cpu = args.cpu_iters or 64
+        cpu = cpu_sample(small, n_cpu, "C5 generator at 1/50 scale", "c2")
+        ratio = lp.nnz / small.nnz
+        cpu["value"] /= ratio
+        cpu["setup_seconds"] *= ratio
+        cpu["sample"] = (f"the reference on the C5 generator at m={small.num_cons}, "
+                         f"n={small.num_vars}, {small.nnz} nnz (setup + {n_cpu} iterations, "
+                         f"1 thread); iter/s and setup extrapolated linearly in nonzeros "
+                         f"(x{ratio:.1f})")
+    else:
+        n_cpu = args.cpu_iters if args.cpu_iters else (8 if args.config in BOUNDED else 64)
+        cpu = cpu_sample(lp, n_cpu, WORKLOADS[args.config], args.config)
+    if e2e and e2e["status"] == "optimal":
+        it = e2e["iterations"]
+        cpu["time_to_tol_extrapolated_s"] = cpu["setup_seconds"] + it / cpu["value"]
+        cpu["extrapolation"] = (f"setup + {it} iterations (the GPU's count to {args.e2e_eps}) "
+                                "/ sampled reference iter/s")
+        if e2e.get("iterations_to_1e-4"):
+            cpu["time_to_1e-4_extrapolated_s"] = (cpu["setup_seconds"] +
+                                                  e2e["iterations_to_1e-4"] / cpu["value"])
+        cpu["time_to_tol_speedup_vs_e2e"] = cpu["time_to_tol_extrapolated_s"] / e2e["time_to_tol_s"]
+    return cpu
+
+
 # ------------------------------------------------------------------ parity ---
 def parity_block(lp, config, e2e_x, e2e_y, e2e_tol):
     """Outside every timed region: (1) the e2e solution re-checked by the
@@ -503,33 +533,18 @@ def run_product(args):
 
     cpu = None
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
-        if args.config == "c5":
-            small = generators.c5_rowpart(**C5_CPU_SAMPLE)
-            cpu = cpu_sample(small, args.cpu_iters or 64, "C5 generator at 1/50 scale", "c2")
-            ratio = lp.nnz / small.nnz
-            cpu["value"] /= ratio
-            cpu["setup_seconds"] *= ratio
-            cpu["sample"] = (f"the reference on the C5 generator at m={small.num_cons}, "
-                             f"n={small.num_vars}, {small.nnz} nnz (setup + {args.cpu_iters or 64} "
-                             f"iterations, 1 thread); iter/s and setup extrapolated linearly in "
-                             f"nonzeros (x{ratio:.1f})")
-        else:
-            n_cpu = args.cpu_iters if args.cpu_iters else (8 if args.config in BOUNDED else 64)
-            cpu = cpu_sample(lp, n_cpu, WORKLOADS[args.config], args.config)
-        if e2e and e2e["status"] == "optimal":
-            it = e2e["iterations"]
-            cpu["time_to_tol_extrapolated_s"] = cpu["setup_seconds"] + it / cpu["value"]
-            cpu["extrapolation"] = (f"setup + {it} iterations (the GPU's count to {args.e2e_eps}) "
-                                    "/ sampled reference iter/s")
-            if e2e.get("iterations_to_1e-4"):
-                cpu["time_to_1e-4_extrapolated_s"] = (cpu["setup_seconds"] +
-                                                      e2e["iterations_to_1e-4"] / cpu["value"])
-            cpu["time_to_tol_speedup_vs_e2e"] = cpu["time_to_tol_extrapolated_s"] / e2e["time_to_tol_s"]
+        try:  # a baseline failure must not cost the measured line
+            cpu = cpu_baseline_leg(args, lp, e2e)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"error": f"{type(exc).__name__}: {exc}"}
 
     parity = None
     if not args.no_parity and dist.rank == 0 and dist.world == 1 and args.config != "c5":
-        parity = parity_block(lp, args.config, e2e_sol[0] if e2e_sol else None,
-                              e2e_sol[1] if e2e_sol else None, args.e2e_eps)
+        try:  # a checker failure must not cost the measured line
+            parity = parity_block(lp, args.config, e2e_sol[0] if e2e_sol else None,
+                                  e2e_sol[1] if e2e_sol else None, args.e2e_eps)
+        except Exception as exc:  # noqa: BLE001
+            parity = {"error": f"{type(exc).__name__}: {exc}"}
 
     if dist.rank == 0:
         line = {

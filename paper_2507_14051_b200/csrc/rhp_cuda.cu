@@ -485,8 +485,14 @@ __global__ void __launch_bounds__(256) k_gather_probe(const int32_t* __restrict_
 // longest row has <= kThreadRowMax nonzeros, else the merge-path warp engine.
 // RHP_THREAD_ROWS=0 forces merge path; =1 allows rows up to 64 nonzeros.
 void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
+  // RHP_THREAD_ROWS: 0 forces the merge path, 1 allows rows up to 64, a
+  // larger number is the cap itself (A/B runs)
   const char* env = std::getenv("RHP_THREAD_ROWS");
-  const int64_t cap = env && env[0] == '0' ? -1 : env && env[0] == '1' ? 64 : kThreadRowMax;
+  int64_t cap = kThreadRowMax;
+  if (env) {
+    const long v = std::atol(env);
+    cap = v == 0 ? -1 : v == 1 ? 64 : v;
+  }
   const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
   int64_t longest = 0;
   for (int64_t r = 0; r < rows; ++r) longest = std::max(longest, rp[r + 1] - rp[r]);

@@ -218,8 +218,9 @@ int rhpdhg_session_gather_ceiling(rhpdhg_session* s, int reps, double* ms2);
  * uses the thread-per-row engine, bit 1: A^T), then the column segment
  * counts (A's in bits 0-15, A^T's in bits 16-31), then 1 when blocks run as
  * the cluster-resident kernel, then the partition mode (0 single GPU,
- * 1 row-partitioned with a replicated n-side walk, 2 sharded). */
-int rhpdhg_session_layout(rhpdhg_session* s, int64_t* out29);
+ * 1 row-partitioned with a replicated n-side walk, 2 sharded), then the
+ * constant-bound bits (bit 0 var_lb, 1 var_ub, 2 con_lb, 3 con_ub). */
+int rhpdhg_session_layout(rhpdhg_session* s, int64_t* out30);
 int rhpdhg_session_finish(rhpdhg_session* s, rhpdhg_report_c* report, double* x, double* y,
                           double* reduced_costs, double* history, int64_t history_cap);
 void rhpdhg_session_destroy(rhpdhg_session* s);

@@ -147,6 +147,8 @@ typedef struct rhp_layout_info {
   int32_t resident;     /* blocks run as one cluster-resident kernel (small LPs) */
   int32_t partition;    /* 0 single GPU, 1 row-partitioned with replicated n-side walk
                            (Option A: allreduce / peer exchange), 2 sharded (Option B) */
+  int32_t const_bounds; /* bounds constant after scaling, taken from kernel parameters instead of
+                           loaded: bit 0 var_lb, 1 var_ub, 2 con_lb, 3 con_ub */
 } rhp_layout_info;
 
 const char* rhp_last_error(void);

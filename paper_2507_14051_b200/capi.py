@@ -180,7 +180,7 @@ class RhpLayoutInfo(C.Structure):
         ("grid_a", C.c_int32), ("grid_at", C.c_int32), ("grid_vec", C.c_int32),
         ("sm_count", C.c_int32), ("gather_l1", C.c_int32), ("pdl", C.c_int32),
         ("thread_rows", C.c_int32), ("segments", C.c_int32),
-        ("resident", C.c_int32), ("partition", C.c_int32),
+        ("resident", C.c_int32), ("partition", C.c_int32), ("const_bounds", C.c_int32),
     ]
 
 

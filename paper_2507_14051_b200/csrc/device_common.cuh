@@ -17,6 +17,13 @@
 
 namespace rhp {
 
+// Per-epilogue constant inputs (spmv.cuh load_inputs): bit k of mask set ->
+// input k equals val[k] on every row.
+struct ConstInputs {
+  unsigned mask;
+  double val[8];
+};
+
 #ifndef RHP_BLOCK
 #define RHP_BLOCK 256
 #endif

@@ -72,6 +72,7 @@ struct EpiPrimal {
   Ctl* ctl;
   PrimalOut o;
   const double* in[NIN];
+  ConstInputs cin;  // constant inputs (bounds), not loaded
   double a, b, g, opg, tau;
   __device__ bool enter() {
     const int64_t k = ctl->k;
@@ -170,6 +171,7 @@ struct EpiDual {
   double* ax;
   double* yplus;
   const double* in[NIN];
+  ConstInputs cin;  // constant inputs (bounds), not loaded
   const double* part3;     // primal partials [4][grid3]
   int grid3;
   int n_multi3;            // multi-chunk rows of the A^T schedule and their
@@ -268,6 +270,7 @@ struct EpiAtyDist {
   double* aty;
   PrimalOut o;
   const double* in[NIN];
+  ConstInputs cin;  // constant inputs (bounds), not loaded
   int token;
   double a, b, a2, b2, g, opg, tau;
   int stop;
@@ -305,6 +308,7 @@ struct EpiAty {
   double* aty;
   PrimalOut o;
   const double* in[NIN];
+  ConstInputs cin;  // constant inputs (bounds), not loaded
   int token;
   int guard;  // graph copy > 0 of an unrolled body: run only after its own K1
   double a, b, a2, b2, g, opg, tau;

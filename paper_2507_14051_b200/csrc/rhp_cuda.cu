@@ -249,6 +249,11 @@ struct rhp_ctx {
   int32_t *res_a_split = nullptr, *res_at_split = nullptr;
   bool pdl = false;  // programmatic dependent launch of the SpMVs (launch_spmv, RHP_PDL=1)
   bool scaled = false;  // rhp_scale ran (it consumes the original values: once per ctx)
+  // bounds that are one value on every row / column after scaling (bit 0
+  // var_lb, 1 var_ub, 2 con_lb, 3 con_ub) and those values: the epilogues
+  // take them from kernel parameters instead of loading them (ConstInputs)
+  unsigned const_mask = 0;
+  double const_val[4] = {0, 0, 0, 0};
   // per-operation API scratch (rhp_op_pdhg), allocated on first use:
   // 12 n-vectors then 11 m-vectors
   double* opbuf = nullptr;
@@ -442,6 +447,40 @@ int prepare_spmv() {
 }
 
 PrimalOut primal_out(rhp_ctx& c) { return PrimalOut{c.x, c.xp}; }
+
+// Marks epilogue input k constant when bound `which` (0 vl, 1 vu, 2 cl, 3 cu)
+// is constant (rhp_ctx::const_mask).
+void mark_const(const rhp_ctx& c, ConstInputs& ci, int k, int which) {
+  if ((c.const_mask >> which) & 1u) {
+    ci.mask |= 1u << k;
+    ci.val[k] = c.const_val[which];
+  }
+}
+
+// rhp_ctx::const_mask of the final (scaled) bounds; RHP_CONST_INPUTS=0
+// disables it (A/B). Decided per rank from its own vectors: it only selects
+// where a value is read from, never the value.
+void detect_constant_inputs(rhp_ctx& c) {
+  c.const_mask = 0;
+  if (const char* e = std::getenv("RHP_CONST_INPUTS"); e && std::atoi(e) == 0) return;
+  const double* vec[4] = {c.vl, c.vu, c.cl, c.cu};
+  const int64_t len[4] = {c.n, c.n, c.m, c.m};
+  unsigned* flags = dev_alloc<unsigned>(4);
+  CK(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned), c.stream));
+  for (int q = 0; q < 4; ++q)
+    if (len[q] > 0)
+      k_not_constant<<<vec_grid(c, len[q]), kBlock, 0, c.stream>>>(vec[q], len[q], flags + q);
+  CK(cudaGetLastError());
+  unsigned h[4];
+  CK(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  for (int q = 0; q < 4; ++q)
+    if (len[q] > 0)
+      CK(cudaMemcpyAsync(&c.const_val[q], vec[q], sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaFree(flags));
+  for (int q = 0; q < 4; ++q)
+    if (len[q] > 0 && h[q] == 0) c.const_mask |= 1u << q;
+}
 
 EpiStore store_into(double* out) {
   EpiStore e{};
@@ -762,6 +801,8 @@ EpiDual epi_dual(rhp_ctx& c, int token) {
   e.yplus = c.yp;
   const double* in[] = {c.y, c.ax, c.cl, c.cu, c.y0, c.ax0};
   for (int k = 0; k < EpiDual::NIN; ++k) e.in[k] = in[k];
+  mark_const(c, e.cin, 2, 2);
+  mark_const(c, e.cin, 3, 3);
   e.part3 = c.part3;
   e.grid3 = nside_grid(c);
   e.n_multi3 = nside_sched(c).n_multi;
@@ -777,6 +818,8 @@ EpiAty epi_aty(rhp_ctx& c, int token) {
   e.o = primal_out(c);
   const double* in[] = {c.aty, c.aty0, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiAty::NIN; ++k) e.in[k] = in[k];
+  mark_const(c, e.cin, 4, 0);
+  mark_const(c, e.cin, 5, 1);
   e.token = token;
   return e;
 }
@@ -831,6 +874,8 @@ void launch_iteration(rhp_ctx& c, int token, cudaStream_t s, bool guard = false)
   e.o = primal_out(c);
   const double* in[] = {c.xchg, c.aty, c.aty0, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiAtyDist::NIN; ++k) e.in[k] = in[k];
+  mark_const(c, e.cin, 5, 0);
+  mark_const(c, e.cin, 6, 1);
   e.token = token;
   epilogue_walk<EpiAtyDist><<<nside_grid(c), kBlock, 0, s>>>(nside_sched(c), e, c.part3);
   CK(cudaGetLastError());
@@ -867,6 +912,8 @@ void launch_iteration_sharded(rhp_ctx& c, int token, cudaStream_t s) {
   const double* in[] = {c.rsb, c.aty + lo, c.aty0 + lo, c.x + lo, c.c + lo, c.vl + lo, c.vu + lo,
                         c.x0 + lo};
   for (int k = 0; k < EpiAtyDist::NIN; ++k) e.in[k] = in[k];
+  mark_const(c, e.cin, 5, 0);
+  mark_const(c, e.cin, 6, 1);
   e.token = token;
   epilogue_walk<EpiAtyDist><<<c.grid_nside, kBlock, 0, s>>>(c.nside, e, c.part3);
   CK(cudaGetLastError());
@@ -962,6 +1009,8 @@ void launch_resident(rhp_ctx& c, cudaStream_t s) {
   p.primal.o = primal_out(c);
   const double* in[] = {c.aty, c.x, c.c, c.vl, c.vu, c.x0};
   for (int k = 0; k < EpiPrimal::NIN; ++k) p.primal.in[k] = in[k];
+  mark_const(c, p.primal.cin, 3, 0);
+  mark_const(c, p.primal.cin, 4, 1);
   p.ctl = c.ctl;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(c.res_ctas));
@@ -985,6 +1034,8 @@ void launch_primal_init(rhp_ctx& c, cudaStream_t s) {
   e.o = PrimalOut{c.x + lo, c.xp + lo};
   const double* in[] = {c.aty + lo, c.x + lo, c.c + lo, c.vl + lo, c.vu + lo, c.x0 + lo};
   for (int k = 0; k < EpiPrimal::NIN; ++k) e.in[k] = in[k];
+  mark_const(c, e.cin, 3, 0);
+  mark_const(c, e.cin, 4, 1);
   epilogue_walk<EpiPrimal><<<nside_grid(c), kBlock, 0, s>>>(nside_sched(c), e, c.part3);
   CK(cudaGetLastError());
   if (c.sharded) sharded_walk_tail(c, s);
@@ -1451,6 +1502,7 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
                         (c->A.cta_row ? 4 : 0);
     info->resident = c->resident ? 1 : 0;
     info->partition = !c->dist ? 0 : c->sharded ? 2 : 1;
+    info->const_bounds = static_cast<int32_t>(c->const_mask);
     info->segments = static_cast<int32_t>(std::max<size_t>(1, c->A.segs.size()) |
                                           (std::max<size_t>(1, c->At.segs.size()) << 16));
   });
@@ -1523,6 +1575,7 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
     c->A.v_orig = c->At.v_orig = nullptr;
     if (c->csc_src) CK(cudaFree(c->csc_src));
     c->csc_src = nullptr;
+    detect_constant_inputs(*c);
     // column segments of the scaled operators (gathered vectors larger than L2)
     build_segments(*c, c->A, c->L.A, c->n, c->grid_a);
     build_segments(*c, c->At, c->L.At, c->m, c->grid_at);

@@ -40,6 +40,17 @@ __global__ void k_vec_div(double* s, const double* by, int64_t n) {
     s[i] = __ddiv_rn(s[i], by[i]);
 }
 
+// flag[0] |= 1 unless every v[i] equals v[0] bitwise (constant-input
+// detection for the epilogues, rhp_cuda.cu detect_constant_inputs)
+__global__ void k_not_constant(const double* v, int64_t n, unsigned* flag) {
+  const unsigned long long v0 = __double_as_longlong(v[0]);
+  bool diff = false;
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kBlock)
+    diff |= static_cast<unsigned long long>(__double_as_longlong(v[i])) != v0;
+  if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
 __global__ void k_vec_mul(double* s, const double* by, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * kBlock)

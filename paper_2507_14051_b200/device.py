@@ -63,7 +63,9 @@ class DeviceContext:
                 "pdl": bool(info.pdl),
                 "thread_rows": {"A": bool(info.thread_rows & 1), "At": bool(info.thread_rows & 2)},
                 "segments": {"A": info.segments & 0xffff, "At": info.segments >> 16},
-                "resident": bool(info.resident)}
+                "resident": bool(info.resident),
+                "const_bounds": [k for b, k in enumerate(("var_lb", "var_ub", "con_lb", "con_ub"))
+                                 if (info.const_bounds >> b) & 1]}
 
     def scale(self, enabled=True, ruiz=10, pock_chambolle=True):
         self._ok(self.lib.rhp_scale(self.h, int(enabled), ruiz, int(pock_chambolle)))

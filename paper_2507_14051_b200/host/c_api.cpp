@@ -300,6 +300,7 @@ int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
     o[26] = li.segments;
     o[27] = li.resident;
     o[28] = li.partition;
+    o[29] = li.const_bounds;
   });
 }
 

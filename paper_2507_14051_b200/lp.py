@@ -504,7 +504,7 @@ class Session:
         return {"A": ms[0], "At": ms[1]}
 
     def layout(self) -> dict:
-        o = (C.c_int64 * 29)()
+        o = (C.c_int64 * 30)()
         self._check(self._lib.rhpdhg_session_layout(self._h, o))
         return {"m": o[0], "n": o[1], "nnz": o[2], "row_bins": list(o[3:11]),
                 "col_bins": list(o[11:19]), "grid_a": o[19], "grid_at": o[20],
@@ -514,7 +514,9 @@ class Session:
                 "cta_rows": {"A": bool(o[25] & 4)},
                 "segments": {"A": int(o[26] & 0xffff), "At": int(o[26] >> 16)},
                 "resident": bool(o[27]),
-                "partition": {0: "single", 1: "replicated", 2: "sharded"}[int(o[28])]}
+                "partition": {0: "single", 1: "replicated", 2: "sharded"}[int(o[28])],
+                "const_bounds": [k for b, k in enumerate(("var_lb", "var_ub", "con_lb", "con_ub"))
+                                 if (o[29] >> b) & 1]}
 
     def finish(self) -> SolutionReport:
         def fn(view, cc, rep, x, y, rc_, hist, cap):

@@ -414,3 +414,48 @@ def test_device_kkt_counts_nan_iterates(gpu):
         dev.set_iterate([float("nan")], [0.0])
         s = dev.kkt(0)
     assert s["nan_x"] == 1
+
+
+def const_bound_lps():
+    t = c3_transport(S=40, T=70)  # x >= 0, no upper bounds: both variable bounds constant
+    # every bound constant (and kept constant: scaling off below)
+    r = random_rows_lp(3, 300, 400, np.random.default_rng(2).integers(1, 30, 300))
+    r = LpProblem(r.num_cons, r.num_vars, r.row_ptr, r.col_index, r.values, r.objective,
+                  [-1.0] * r.num_vars, [2.0] * r.num_vars, [-3.0] * r.num_cons,
+                  [math.inf] * r.num_cons)
+    return [("transport", t, True, ["var_lb", "var_ub"]),
+            ("all_constant_unscaled", r, False, ["var_lb", "var_ub", "con_lb", "con_ub"])]
+
+
+@pytest.mark.parametrize("rows", ["0", "1"], ids=["merge_path", "thread_rows"])
+@pytest.mark.parametrize("case", const_bound_lps(), ids=lambda c: c[0])
+def test_constant_bounds_are_parameters_and_change_nothing(gpu, case, rows, monkeypatch):
+    """Bounds that are one value on every row / column after scaling are
+    passed to the epilogues as kernel parameters instead of loaded
+    (ConstInputs, rhp_cuda.cu detect_constant_inputs): detected as such, and
+    the solve is bitwise the one that loads them (RHP_CONST_INPUTS=0), in
+    graph and plain launches."""
+    from paper_2507_14051_b200.lp import set_resident
+
+    _, lp, scaling, want = case
+    monkeypatch.setenv("RHP_THREAD_ROWS", rows)
+    with DeviceContext(lp) as dev:
+        dev.scale(enabled=scaling)
+        assert dev.layout()["const_bounds"] == want
+    cfg = SolverConfig(epsilon=1e-7, scaling_enabled=scaling)
+    out = {}
+    try:
+        set_resident(0)  # the multi-CTA engines (the resident kernel stages whole vectors)
+        for flag in ("1", "0"):
+            monkeypatch.setenv("RHP_CONST_INPUTS", flag)
+            for graph in (True, False):
+                set_device_options(use_graph=graph)
+                out[flag, graph] = solve(lp, cfg)
+    finally:
+        set_resident(-1)
+        set_device_options()
+    base = out["0", True]
+    assert base.status == "optimal"
+    for r in out.values():
+        assert r.iterations == base.iterations
+        assert np.array_equal(r.x, base.x) and np.array_equal(r.y, base.y)

@@ -215,7 +215,9 @@ int rhpdhg_session_gather_ceiling(rhpdhg_session* s, int reps, double* ms2);
  * bin (8 each), the grids of the A, A^T and vector kernels, the SM count,
  * the gather cache policy (bit 0: A through L1, bit 1: A^T) and whether the
  * SpMVs use programmatic dependent launch, then the engine bits (bit 0: A
- * uses the thread-per-row engine, bit 1: A^T), then the column segment
+ * uses the thread-per-row engine, bit 1: A^T, bit 2: A uses the long-row
+ * engine, bits 3 / 4: A / A^T read their sliced copy, bits 5 / 6: A / A^T
+ * have uniform row lengths), then the column segment
  * counts (A's in bits 0-15, A^T's in bits 16-31), then 1 when blocks run as
  * the cluster-resident kernel, then the partition mode (0 single GPU,
  * 1 row-partitioned with a replicated n-side walk, 2 sharded), then the

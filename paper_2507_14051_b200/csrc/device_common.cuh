@@ -98,6 +98,9 @@ __device__ __forceinline__ void pdl_trigger() {
 
 // Merge-path engine: load a window's epilogue inputs (rows r .. r+31) before
 // its gathers (spmv.cuh chunk_range). Off by default (A/B variant).
+#ifndef RHP_UNIFORM_ROWS
+#define RHP_UNIFORM_ROWS 1  // thread-per-row: arithmetic row starts for uniform rows (spmv.cuh)
+#endif
 #ifndef RHP_EPI_PREFETCH
 #define RHP_EPI_PREFETCH 0
 #endif
@@ -203,6 +206,16 @@ struct Sched {
   double* long_red;           // [n_multi * 16] epilogue reductions of split rows
   const double* seg_in;       // column-segmented operators (segments.cuh): running row sums of the
                               // previous segments, added to every row sum before its epilogue; else null
+  // thread-per-row operators whose rows all have the same length (C3's and
+  // C4's A^T): row i starts at i * uniform_len, no row pointers are read
+  // (rhp_cuda.cu apply_engine_rule); 0 -> row pointers
+  int32_t uniform_len;
+  // with uniform_len: the same nonzeros in 32-row slices stored
+  // element-major (element t of row i at (i / 32) * 32 * uniform_len + 32 t
+  // + i % 32: one coalesced load per element position of a warp's 32 rows);
+  // null -> CSR order (rhp_cuda.cu build_sliced, RHP_SLICED=1)
+  const int32_t* sell_ci;
+  const double* sell_v;
 };
 
 struct Csr {

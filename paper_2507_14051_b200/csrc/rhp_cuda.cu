@@ -170,6 +170,9 @@ struct DevOp : DeviceCsr {
   // intermediate segment stores its band-local row sums at seg_out
   int64_t seg_rb = 0, seg_re = 0;
   double* seg_out = nullptr;
+  // sliced copy of a uniform thread-per-row operator (Sched::sell_*, build_sliced)
+  int32_t* sell_ci = nullptr;
+  double* sell_v = nullptr;
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
 
@@ -313,7 +316,8 @@ void free_op(DevOp& d) {
   for (void* p : {(void*)d.rp, (void*)d.ci, (void*)d.v, (void*)d.v_orig, (void*)d.warp_row,
                   (void*)d.warp_nz, (void*)d.slot_row, (void*)d.head_slot, (void*)d.tail_slot,
                   (void*)d.slot_first, (void*)d.slot_count, (void*)d.slot_part,
-                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.segbuf, (void*)d.cta_row})
+                  (void*)d.long_red, (void*)d.slot_ticket, (void*)d.segbuf, (void*)d.cta_row,
+                  (void*)d.sell_ci, (void*)d.sell_v})
     if (p) cudaFree(p);
   d = DevOp{};
 }
@@ -538,6 +542,11 @@ void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
   if (rows > 0 && longest <= cap) {
     d.sched.thread_rows = 1;
     d.sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
+    // every row of one length: row starts are arithmetic (RHP_UNIFORM=0 off)
+    const char* u = std::getenv("RHP_UNIFORM");
+    if (rp[0] == 0 && rp[rows] == rows * longest && longest > 0 && (!u || std::atoi(u) != 0) &&
+        rp[rows] <= INT64_MAX / 32)
+      d.sched.uniform_len = static_cast<int32_t>(longest);
   }
 }
 
@@ -576,6 +585,26 @@ void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp) {
   CK(cudaStreamSynchronize(c.stream));
   d.sched.thread_rows = 0;
   d.sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
+}
+
+// Sliced copy of an unsegmented uniform-length thread-per-row operator's
+// (final, scaled) values: 32-row slices, element-major (Sched::sell_ci).
+// Same elements, same order per row: bit-identical row sums. Off unless
+// RHP_SLICED=1 — measured slower than CSR order.
+void build_sliced(rhp_ctx& c, DevOp& d) {
+  const char* e = std::getenv("RHP_SLICED");
+  if (!e || std::atoi(e) == 0) return;
+  if (!d.segs.empty() || !d.sched.thread_rows || d.sched.uniform_len <= 0 || d.nnz == 0) return;
+  const int64_t rows = d.rows, w = d.sched.uniform_len;
+  const size_t cap = static_cast<size_t>((rows + 31) / 32 * 32 * w);
+  d.sell_ci = dev_alloc<int32_t>(cap);
+  d.sell_v = dev_alloc<double>(cap);
+  k_build_sliced<<<vec_grid(c, rows), kBlock, 0, c.stream>>>(d.ci, d.v, rows, static_cast<int>(w),
+                                                              d.sell_ci, d.sell_v);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c.stream));
+  d.sched.sell_ci = d.sell_ci;
+  d.sched.sell_v = d.sell_v;
 }
 
 void choose_engines(rhp_ctx& c) {
@@ -1499,7 +1528,9 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->gather_l1 = (c->A.l1g ? 1 : 0) | (c->At.l1g ? 2 : 0);
     info->pdl = c->pdl ? 1 : 0;
     info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0) |
-                        (c->A.cta_row ? 4 : 0);
+                        (c->A.cta_row ? 4 : 0) | (fin(c->A).sell_ci ? 8 : 0) |
+                        (fin(c->At).sell_ci ? 16 : 0) | (fin(c->A).sched.uniform_len ? 32 : 0) |
+                        (fin(c->At).sched.uniform_len ? 64 : 0);
     info->resident = c->resident ? 1 : 0;
     info->partition = !c->dist ? 0 : c->sharded ? 2 : 1;
     info->const_bounds = static_cast<int32_t>(c->const_mask);
@@ -1579,6 +1610,8 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
     // column segments of the scaled operators (gathered vectors larger than L2)
     build_segments(*c, c->A, c->L.A, c->n, c->grid_a);
     build_segments(*c, c->At, c->L.At, c->m, c->grid_at);
+    build_sliced(*c, c->A);
+    build_sliced(*c, c->At);
     if (c->graph_built) {  // the block graph captured the unsegmented launches
       CK(cudaGraphExecDestroy(c->gexec));
       CK(cudaGraphDestroy(c->graph));

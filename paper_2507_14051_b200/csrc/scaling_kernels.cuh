@@ -40,6 +40,20 @@ __global__ void k_vec_div(double* s, const double* by, int64_t n) {
     s[i] = __ddiv_rn(s[i], by[i]);
 }
 
+// Sliced copy of a uniform-length (w) CSR operator (rhp_cuda.cu
+// build_sliced): element t of row i to (i / 32) * 32 w + 32 t + i % 32.
+__global__ void k_build_sliced(const int32_t* ci, const double* v, int64_t rows, int w,
+                               int32_t* sci, double* sv) {
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * kBlock) {
+    const int64_t o = (i >> 5) * 32 * w + (i & 31);
+    for (int t = 0; t < w; ++t) {
+      sci[o + 32 * t] = ci[i * w + t];
+      sv[o + 32 * t] = v[i * w + t];
+    }
+  }
+}
+
 // flag[0] |= 1 unless every v[i] equals v[0] bitwise (constant-input
 // detection for the epilogues, rhp_cuda.cu detect_constant_inputs)
 __global__ void k_not_constant(const double* v, int64_t n, unsigned* flag) {

@@ -234,6 +234,10 @@ __device__ __forceinline__ void chunk_range(const int w, const int32_t* ci, cons
           p[t] = add(excl, p[t]);
         }
       }
+      // every value is stored, though only the row ends are read back:
+      // storing just those (predicated stores, a shuffle for the next lane's
+      // first flag) cut the shared-store wavefronts but cost more issue
+      // slots (C4 K1 688 -> 699 us, C2 K1 70.2 -> 70.8 us)
 #pragma unroll
       for (int t = 0; t < kPer; ++t) sm.val[sv(kPer * lane + t)] = p[t];
       __syncwarp();
@@ -333,7 +337,8 @@ __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* val
   // whatever RF is, so the reductions do not depend on RF
   for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x; i0 < R; i0 += RF * G) {
     double e[RF][NI], sm[RF];
-    int64_t lo[RF], hi[RF];
+    int64_t lo[RF];
+    int len[RF];
 #pragma unroll
     for (int f = 0; f < RF; ++f) {
       const int64_t i = i0 + f * G;
@@ -341,35 +346,52 @@ __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* val
       sm[f] = 0.0;
     }
     if constexpr (!WALK) {
-      int64_t len = 0;
+      // sliced copy (coalesced element loads, 1-B lengths instead of row
+      // pointers) when built, else CSR; same elements in the same order
+#if RHP_UNIFORM_ROWS
+      const int w = s.uniform_len;
+      const bool sliced = s.sell_ci != nullptr;
+#else  // A/B variant: the row-pointer path only
+      constexpr int w = 0;
+      constexpr bool sliced = false;
+#endif
+      const int32_t* cix = sliced ? s.sell_ci : ci;
+      const double* vx = sliced ? s.sell_v : vals;
+      const int64_t es = sliced ? 32 : 1;  // element stride of a row
+      int lmax = 0;
 #pragma unroll
       for (int f = 0; f < RF; ++f) {
         const int64_t i = i0 + f * G;
-        lo[f] = i < R ? s.rp[i] : 0;
-        hi[f] = i < R ? s.rp[i + 1] : 0;
-        len = max(len, hi[f] - lo[f]);
+        if (w > 0) {  // no row-pointer round before the index loads
+          lo[f] = sliced ? (i >> 5) * (32 * static_cast<int64_t>(w)) + (i & 31) : i * w;
+          len[f] = i < R ? w : 0;
+        } else {
+          lo[f] = i < R ? s.rp[i] : 0;
+          len[f] = i < R ? static_cast<int>(s.rp[i + 1] - lo[f]) : 0;
+        }
+        lmax = max(lmax, len[f]);
       }
-      for (int64_t t = 0; t < len; t += EC) {
+      for (int t = 0; t < lmax; t += EC) {
         int c[RF][EC];
         double v[RF][EC], g[RF][EC];
 #pragma unroll
         for (int f = 0; f < RF; ++f)
 #pragma unroll
           for (int u = 0; u < EC; ++u) {
-            const bool ok = lo[f] + t + u < hi[f];
-            c[f][u] = ok ? __ldcs(ci + lo[f] + t + u) : 0;
-            v[f][u] = ok ? __ldcs(vals + lo[f] + t + u) : 0.0;
+            const bool ok = t + u < len[f];
+            c[f][u] = ok ? __ldcs(cix + lo[f] + (t + u) * es) : 0;
+            v[f][u] = ok ? __ldcs(vx + lo[f] + (t + u) * es) : 0.0;
           }
 #pragma unroll
         for (int f = 0; f < RF; ++f)
 #pragma unroll
           for (int u = 0; u < EC; ++u)
-            g[f][u] = lo[f] + t + u < hi[f] ? ld_gather<L1G>(xg + c[f][u]) : 0.0;
+            g[f][u] = t + u < len[f] ? ld_gather<L1G>(xg + c[f][u]) : 0.0;
 #pragma unroll
         for (int f = 0; f < RF; ++f)
 #pragma unroll
           for (int u = 0; u < EC; ++u)
-            if (lo[f] + t + u < hi[f]) sm[f] = add(sm[f], mul(v[f][u], g[f][u]));
+            if (t + u < len[f]) sm[f] = add(sm[f], mul(v[f][u], g[f][u]));
       }
       if (s.seg_in) {
 #pragma unroll

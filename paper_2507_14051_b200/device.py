@@ -62,6 +62,9 @@ class DeviceContext:
                 "gather_l1": {"A": bool(info.gather_l1 & 1), "At": bool(info.gather_l1 & 2)},
                 "pdl": bool(info.pdl),
                 "thread_rows": {"A": bool(info.thread_rows & 1), "At": bool(info.thread_rows & 2)},
+                "sliced": {"A": bool(info.thread_rows & 8), "At": bool(info.thread_rows & 16)},
+                "uniform_rows": {"A": bool(info.thread_rows & 32),
+                                 "At": bool(info.thread_rows & 64)},
                 "segments": {"A": info.segments & 0xffff, "At": info.segments >> 16},
                 "resident": bool(info.resident),
                 "const_bounds": [k for b, k in enumerate(("var_lb", "var_ub", "con_lb", "con_ub"))

@@ -512,6 +512,8 @@ class Session:
                 "gather_l1": {"A": bool(o[23] & 1), "At": bool(o[23] & 2)}, "pdl": bool(o[24]),
                 "thread_rows": {"A": bool(o[25] & 1), "At": bool(o[25] & 2)},
                 "cta_rows": {"A": bool(o[25] & 4)},
+                "sliced": {"A": bool(o[25] & 8), "At": bool(o[25] & 16)},
+                "uniform_rows": {"A": bool(o[25] & 32), "At": bool(o[25] & 64)},
                 "segments": {"A": int(o[26] & 0xffff), "At": int(o[26] >> 16)},
                 "resident": bool(o[27]),
                 "partition": {0: "single", 1: "replicated", 2: "sharded"}[int(o[28])],

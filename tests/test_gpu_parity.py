@@ -459,3 +459,56 @@ def test_constant_bounds_are_parameters_and_change_nothing(gpu, case, rows, monk
     for r in out.values():
         assert r.iterations == base.iterations
         assert np.array_equal(r.x, base.x) and np.array_equal(r.y, base.y)
+
+
+@pytest.mark.parametrize("case", ["transport", "uniform_rows_A", "ragged_short_rows"])
+def test_uniform_and_sliced_rows_are_bitwise_the_csr_path(gpu, case, monkeypatch):
+    """Thread-per-row operators whose rows all have one length skip the
+    row-pointer reads (row i starts at i * len; rhp_cuda.cu
+    apply_engine_rule), and with RHP_SLICED=1 read a sliced copy (32-row
+    slices, element-major; build_sliced): SpMVs and solves bitwise equal to
+    the row-pointer path (RHP_UNIFORM=0) — same elements, same order — with a
+    row count that is not a multiple of 32; ragged rows keep row pointers."""
+    from paper_2507_14051_b200.lp import set_resident
+
+    rng = np.random.default_rng(4)
+    if case == "transport":
+        lp, which = c3_transport(S=40, T=70), "At"
+    elif case == "uniform_rows_A":  # 1001 rows of exactly 5 distinct columns, box bounds
+        m, n = 1001, 777
+        cols = np.sort((np.arange(m)[:, None] * 7 + np.arange(5)[None, :] * 131) % n, axis=1)
+        lp = LpProblem(m, n, np.arange(0, 5 * m + 1, 5), cols.ravel(),
+                       rng.uniform(0.5, 2.0, 5 * m) * rng.choice([-1.0, 1.0], 5 * m),
+                       rng.uniform(-1, 1, n), [-1.0] * n, [1.0] * n, [-10.0] * m, [3.0] * m)
+        which = "A"
+    else:
+        lp, which = random_rows_lp(7, 1001, 777, rng.integers(0, 9, 1001)), None
+    x, y = rng.uniform(-1, 1, lp.num_vars), rng.uniform(-1, 1, lp.num_cons)
+    got = {}
+    for mode, env in (("csr", {"RHP_UNIFORM": "0"}), ("uniform", {}), ("sliced", {"RHP_SLICED": "1"})):
+        monkeypatch.delenv("RHP_UNIFORM", raising=False)
+        monkeypatch.delenv("RHP_SLICED", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with DeviceContext(lp) as dev:
+            dev.scale()
+            lay = dev.layout()
+            got[mode, "spmv"] = (dev.spmv(x), dev.spmv(y, True))
+        if which:
+            assert lay["uniform_rows"][which] == (mode != "csr")
+            assert lay["sliced"][which] == (mode == "sliced")
+        else:
+            assert not any(lay["uniform_rows"].values()) or not lay["thread_rows"]["A"]
+        try:
+            set_resident(0)
+            got[mode, "solve"] = solve(lp, SolverConfig(epsilon=1e-7))
+        finally:
+            set_resident(-1)
+    base = got["csr", "solve"]
+    assert base.status == "optimal"
+    for mode in ("uniform", "sliced"):
+        for a, b in zip(got[mode, "spmv"], got["csr", "spmv"]):
+            assert np.array_equal(a, b), mode
+        r = got[mode, "solve"]
+        assert r.iterations == base.iterations, mode
+        assert np.array_equal(r.x, base.x) and np.array_equal(r.y, base.y), mode

@@ -157,18 +157,23 @@ class Dist:
 
 
 # ------------------------------------------------------------ bytes model ----
-def algorithmic_bytes(m, n, nnz, const_bounds=()):
+def algorithmic_bytes(m, n, nnz, const_bounds=(), uniform_rows=None):
     """Per-launch algorithmic HBM bytes of the fused kernels:
     K1: 12 nnz + 8(m+1) row_ptr + 8 n (x+ gathered once) + 72 m (read ax, y,
         lo, hi, y0, ax0; write y+, y, ax)
     K2: 12 nnz + 8(n+1) + 8 m (y+ gathered once) + 24 n (aty, aty0 -> aty)
         + 56 n (read x, c, l, u, x0; write x+, x) = 12 nnz + 8(n+1) + 8 m + 80 n.
     A bound that is one value everywhere (layout const_bounds: C3, C4 x >= 0)
-    is a kernel parameter, not a stream: its 8 m / 8 n bytes are not counted."""
+    is a kernel parameter, not a stream: its 8 m / 8 n bytes are not counted;
+    nor are the row pointers of an operator with uniform row lengths (layout
+    uniform_rows: C3's and C4's A^T), whose row starts are arithmetic."""
     k1 = 12 * nnz + 8 * (m + 1) + 8 * n + 72 * m
     k2 = 12 * nnz + 8 * (n + 1) + 8 * m + 80 * n
     k1 -= 8 * m * sum(b in const_bounds for b in ("con_lb", "con_ub"))
     k2 -= 8 * n * sum(b in const_bounds for b in ("var_lb", "var_ub"))
+    uniform_rows = uniform_rows or {}
+    k1 -= 8 * (m + 1) if uniform_rows.get("A") else 0
+    k2 -= 8 * (n + 1) if uniform_rows.get("At") else 0
     return k1, k2
 
 
@@ -466,7 +471,8 @@ def run_product(args):
     kt = sess.time_kernels(reps=20)
     sess.close()
     # per-GPU algorithmic bytes (local rows / nonzeros on the partitioned path)
-    k1b, k2b = algorithmic_bytes(layout["m"], n, layout["nnz"], layout.get("const_bounds", ()))
+    k1b, k2b = algorithmic_bytes(layout["m"], n, layout["nnz"], layout.get("const_bounds", ()),
+                                 layout.get("uniform_rows"))
     k1 = k1b / (kt["k1_dual_spmv_ms"] * 1e-3) / 1e9
     k2 = k2b / (kt["k2_aty_spmv_primal_ms"] * 1e-3) / 1e9
     dominant = "k2" if kt["k2_aty_spmv_primal_ms"] >= kt["k1_dual_spmv_ms"] else "k1"

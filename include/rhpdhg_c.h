@@ -217,7 +217,8 @@ int rhpdhg_session_gather_ceiling(rhpdhg_session* s, int reps, double* ms2);
  * SpMVs use programmatic dependent launch, then the engine bits (bit 0: A
  * uses the thread-per-row engine, bit 1: A^T, bit 2: A uses the long-row
  * engine, bits 3 / 4: A / A^T read their sliced copy, bits 5 / 6: A / A^T
- * have uniform row lengths), then the column segment
+ * have uniform row lengths, bits 7 / 8: A / A^T run a thread-per-row row
+ * band), then the column segment
  * counts (A's in bits 0-15, A^T's in bits 16-31), then 1 when blocks run as
  * the cluster-resident kernel, then the partition mode (0 single GPU,
  * 1 row-partitioned with a replicated n-side walk, 2 sharded), then the

@@ -144,7 +144,8 @@ typedef struct rhp_layout_info {
   int32_t thread_rows;  /* bit 0: A uses the thread-per-row engine, bit 1: A^T (last segment);
                            bit 2: A uses the long-row (CTA row run) engine; bits 3 / 4: A / A^T
                            read a sliced (32-row, element-major) copy; bits 5 / 6: A / A^T
-                           have uniform row lengths (no row-pointer reads) */
+                           have uniform row lengths (no row-pointer reads); bits 7 / 8: A / A^T
+                           run a thread-per-row row band ahead of the final pass */
   int32_t segments;     /* column segments: A's in bits 0-15, A^T's in bits 16-31 (1 = unsegmented) */
   int32_t resident;     /* blocks run as one cluster-resident kernel (small LPs) */
   int32_t partition;    /* 0 single GPU, 1 row-partitioned with replicated n-side walk

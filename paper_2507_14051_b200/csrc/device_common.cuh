@@ -140,6 +140,15 @@ constexpr int kCtaRowBlocks = RHP_CTA_BLOCKS;  // resident CTAs per SM the kerne
 #ifndef RHP_ROWS_IN_FLIGHT
 #define RHP_ROWS_IN_FLIGHT 2
 #endif
+#ifndef RHP_CONST_INPUTS_KERNEL
+#define RHP_CONST_INPUTS_KERNEL 1  // epilogue inputs may be kernel parameters (ConstInputs)
+#endif
+#ifndef RHP_ROWS_KERNEL_COMBINED
+#define RHP_ROWS_KERNEL_COMBINED 1  // spmv_rows also carries the merge path (spmv.cuh)
+#endif
+#ifndef RHP_UNIFORM_RF
+#define RHP_UNIFORM_RF 1  // rows in flight of the thread-per-row engine on uniform rows
+#endif
 
 // K1/K2 pairs per body of the block graph's WHILE node (one conditional
 // evaluation per body; copies after a stop exit at entry). C2: 2 -> 6893,

@@ -172,6 +172,7 @@ struct DevOp : DeviceCsr {
   double* seg_out = nullptr;
   // sliced copy of a uniform thread-per-row operator (Sched::sell_*, build_sliced)
   int32_t* sell_ci = nullptr;
+  bool row_band = false;  // a thread-per-row row band runs ahead of the final pass (carve_row_band)
   double* sell_v = nullptr;
   Csr csr() const { return Csr{rp, ci, v, rows}; }
 };
@@ -411,6 +412,11 @@ void launch_one(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const E
     else CK(cudaLaunchKernelEx(&cfg, spmv_cta_rows<Epi, false>, op.csr(), xg, op.sched, cr, epi, part, ticket));
     return;
   }
+  if (op.sched.thread_rows) {
+    if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_rows<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
+    else CK(cudaLaunchKernelEx(&cfg, spmv_rows<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
+    return;
+  }
   if (op.l1g) CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, true>, op.csr(), xg, op.sched, epi, part, ticket));
   else CK(cudaLaunchKernelEx(&cfg, spmv_fused<Epi, false>, op.csr(), xg, op.sched, epi, part, ticket));
 }
@@ -446,6 +452,11 @@ int prepare_spmv() {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &b1, reinterpret_cast<const void*>(spmv_fused<Epi, true>), kBlock, dyn));
   b = std::min(b, b1);
+  for (const void* fn : {reinterpret_cast<const void*>(spmv_rows<Epi, false>),
+                         reinterpret_cast<const void*>(spmv_rows<Epi, true>)}) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, fn, kBlock, dyn));
+    b = std::min(b, b1);
+  }
   if (b < 1) throw CudaError("spmv kernel does not fit on an SM");
   return b;
 }
@@ -591,9 +602,9 @@ void apply_cta_rule(rhp_ctx& c, DevOp& d, const std::vector<int64_t>& rp) {
 // (final, scaled) values: 32-row slices, element-major (Sched::sell_ci).
 // Same elements, same order per row: bit-identical row sums. Off unless
 // RHP_SLICED=1 — measured slower than CSR order.
-void build_sliced(rhp_ctx& c, DevOp& d) {
+void build_sliced(rhp_ctx& c, DevOp& d, bool always = false) {
   const char* e = std::getenv("RHP_SLICED");
-  if (!e || std::atoi(e) == 0) return;
+  if (!always && (!e || std::atoi(e) == 0)) return;
   if (!d.segs.empty() || !d.sched.thread_rows || d.sched.uniform_len <= 0 || d.nnz == 0) return;
   const int64_t rows = d.rows, w = d.sched.uniform_len;
   const size_t cap = static_cast<size_t>((rows + 31) / 32 * 32 * w);
@@ -605,6 +616,140 @@ void build_sliced(rhp_ctx& c, DevOp& d) {
   CK(cudaStreamSynchronize(c.stream));
   d.sched.sell_ci = d.sell_ci;
   d.sched.sell_v = d.sell_v;
+}
+
+// Thread-per-row row band (round 2). A merge-path operator may hold a long
+// run of rows of one length w in (kThreadRowMax, 64] whose columns advance
+// with the row at every element position (C4's arc-capacity rows: row e
+// holds x[k*E + e] for the 25 commodities k, so rows e..e+31 read
+// x[k*E + e .. e+31] at element k). Walked one row per thread, a warp's
+// gathers of one element position are then one or two 128-B lines instead
+// of 32 scattered sectors. Such a band is carved out of the final pass into
+// its own segment (thread-per-row, uniform rows, sums stored to segbuf like
+// a column segment's) and the final pass sees those rows as empty and adds
+// their sums. A band's row sums are sequential in element order (the
+// reference's order). Taken when the band holds >= 5 % of the nonzeros and
+// >= 4096 rows, lies outside the column-segment band, and a sample of
+// 32-row slices touches <= 12 distinct 32-B sectors per element position
+// (8 for 32 consecutive doubles; random columns touch ~32). RHP_ROW_BAND=0 disables it, =force
+// skips the size and sector tests (tests).
+void carve_row_band(rhp_ctx& c, DevOp& d, int64_t cols, int grid) {
+  const char* env = std::getenv("RHP_ROW_BAND");
+  if (env && env[0] == '0') return;
+  const bool force = env && std::strcmp(env, "force") == 0;
+  if (d.cta_row || d.rows < 32) return;
+  const bool had_segs = !d.segs.empty();
+  const DevOp& f = had_segs ? d.segs.back() : d;
+  if (f.sched.thread_rows || f.nnz == 0) return;
+  const int64_t rows = f.rows;
+  std::vector<int64_t> rp(static_cast<size_t>(rows) + 1);
+  CK(cudaMemcpyAsync(rp.data(), f.rp, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  // the longest run (by nonzeros) of equal-length rows with kThreadRowMax < w <= 64,
+  // outside the column-segment band
+  int64_t rb = -1, re = -1, w = 0, best = 0;
+  for (int64_t i = 0; i < rows;) {
+    const int64_t L = rp[i + 1] - rp[i];
+    int64_t j = i + 1;
+    while (j < rows && rp[j + 1] - rp[j] == L) ++j;
+    int64_t a = i, b = j;
+    if (had_segs && a < d.seg_re && b > d.seg_rb) {  // keep the part outside [seg_rb, seg_re)
+      if (a >= d.seg_rb) a = std::max(a, d.seg_re);
+      else b = std::min(b, d.seg_rb);
+    }
+    if (L > kThreadRowMax && L <= 64 && b > a && (b - a) * L > best) {
+      best = (b - a) * L;
+      rb = a;
+      re = b;
+      w = L;
+    }
+    i = j;
+  }
+  if (rb < 0 || re - rb < 32) return;
+  if (!force && (re - rb < 4096 || static_cast<double>(best) < 0.05 * static_cast<double>(f.nnz)))
+    return;
+  if (!force) {  // sectors per element position over sampled 32-row slices
+    const int64_t slices = (re - rb) / 32, samples = std::min<int64_t>(64, slices);
+    std::vector<int32_t> buf(static_cast<size_t>(32 * w));
+    double sectors = 0.0;
+    for (int64_t k = 0; k < samples; ++k) {
+      const int64_t r0 = rb + 32 * (slices * k / samples);
+      CK(cudaMemcpyAsync(buf.data(), f.ci + rp[r0], buf.size() * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      for (int64_t t = 0; t < w; ++t) {
+        int32_t sec[32];
+        for (int r = 0; r < 32; ++r) sec[r] = buf[static_cast<size_t>(r * w + t)] >> 2;
+        std::sort(sec, sec + 32);
+        sectors += static_cast<double>(std::unique(sec, sec + 32) - sec);
+      }
+    }
+    if (sectors / static_cast<double>(samples * w) > 12.0) return;
+  }
+  const int64_t eb = rp[rb], ee = rp[re], nb = re - rb;
+  // the band: its rows with all their elements (uniform rows)
+  DevOp band;
+  band.rows = nb;
+  band.nnz = ee - eb;
+  band.rp = dev_alloc<int64_t>(static_cast<size_t>(nb) + 1);
+  band.ci = dev_alloc<int32_t>(static_cast<size_t>(band.nnz));
+  band.v = dev_alloc<double>(static_cast<size_t>(band.nnz));
+  HostOperator hb;
+  hb.rows = nb;
+  hb.nnz = band.nnz;
+  hb.rp.resize(static_cast<size_t>(nb) + 1);
+  for (int64_t r = 0; r <= nb; ++r) hb.rp[r] = r * w;
+  upload(band.rp, hb.rp.data(), hb.rp.size(), c.stream);
+  CK(cudaMemcpyAsync(band.ci, f.ci + eb, band.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+  CK(cudaMemcpyAsync(band.v, f.v + eb, band.nnz * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  // the final pass: every row, the band's rows empty
+  DevOp fin2;
+  fin2.rows = rows;
+  fin2.nnz = f.nnz - band.nnz;
+  HostOperator hf;
+  hf.rows = rows;
+  hf.nnz = fin2.nnz;
+  hf.rp.resize(static_cast<size_t>(rows) + 1);
+  for (int64_t r = 0; r <= rows; ++r) hf.rp[r] = r <= rb ? rp[r] : r <= re ? eb : rp[r] - (ee - eb);
+  fin2.rp = dev_alloc<int64_t>(static_cast<size_t>(rows) + 1);
+  fin2.ci = dev_alloc<int32_t>(static_cast<size_t>(fin2.nnz));
+  fin2.v = dev_alloc<double>(static_cast<size_t>(fin2.nnz));
+  upload(fin2.rp, hf.rp.data(), hf.rp.size(), c.stream);
+  CK(cudaMemcpyAsync(fin2.ci, f.ci, eb * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+  CK(cudaMemcpyAsync(fin2.v, f.v, eb * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  CK(cudaMemcpyAsync(fin2.ci + eb, f.ci + ee, (f.nnz - ee) * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                     c.stream));
+  CK(cudaMemcpyAsync(fin2.v + eb, f.v + ee, (f.nnz - ee) * sizeof(double), cudaMemcpyDeviceToDevice,
+                     c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  hb.cols = hf.cols = cols;
+  for (HostOperator* h : {&hb, &hf}) build_schedule(*h, static_cast<int64_t>(grid) * kWarps, kRowWeight);
+  upload_sched(band, hb, c.stream);
+  upload_sched(fin2, hf, c.stream);
+  band.sched.thread_rows = 1;
+  band.sched.n_multi = 0;
+  band.sched.uniform_len = static_cast<int32_t>(w);
+  apply_engine_rule(fin2, hf.rp);
+  band.l1g = fin2.l1g = d.l1g;
+  if (!d.segbuf) d.segbuf = dev_alloc<double>(static_cast<size_t>(d.rows));
+  band.sched.seg_in = nullptr;  // the band's first and only partial sums
+  band.seg_out = d.segbuf + rb;
+  fin2.sched.seg_in = d.segbuf;
+  band.seg_rb = rb;
+  band.seg_re = re;
+  // element-major slices: a warp's loads of one element position of its 32
+  // rows are one line of indices and two of values (row-major, 25-element
+  // rows put every lane on its own lines: K1 679 -> 747 us on C4)
+  if (!(std::getenv("RHP_ROW_BAND_CSR"))) build_sliced(c, band, true);
+  if (had_segs) {
+    free_op(d.segs.back());
+    d.segs.back() = fin2;
+    d.segs.insert(d.segs.end() - 1, band);
+  } else {
+    d.segs.push_back(band);
+    d.segs.push_back(fin2);
+  }
+  d.row_band = true;
 }
 
 void choose_engines(rhp_ctx& c) {
@@ -1530,7 +1675,8 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->thread_rows = (fin(c->A).sched.thread_rows ? 1 : 0) | (fin(c->At).sched.thread_rows ? 2 : 0) |
                         (c->A.cta_row ? 4 : 0) | (fin(c->A).sell_ci ? 8 : 0) |
                         (fin(c->At).sell_ci ? 16 : 0) | (fin(c->A).sched.uniform_len ? 32 : 0) |
-                        (fin(c->At).sched.uniform_len ? 64 : 0);
+                        (fin(c->At).sched.uniform_len ? 64 : 0) | (c->A.row_band ? 128 : 0) |
+                        (c->At.row_band ? 256 : 0);
     info->resident = c->resident ? 1 : 0;
     info->partition = !c->dist ? 0 : c->sharded ? 2 : 1;
     info->const_bounds = static_cast<int32_t>(c->const_mask);
@@ -1610,6 +1756,8 @@ int rhp_scale(rhp_ctx* c, int enabled, int ruiz_iterations, int pock_chambolle) 
     // column segments of the scaled operators (gathered vectors larger than L2)
     build_segments(*c, c->A, c->L.A, c->n, c->grid_a);
     build_segments(*c, c->At, c->L.At, c->m, c->grid_at);
+    carve_row_band(*c, c->A, c->n, c->grid_a);
+    carve_row_band(*c, c->At, c->m, c->grid_at);
     build_sliced(*c, c->A);
     build_sliced(*c, c->At);
     if (c->graph_built) {  // the block graph captured the unsegmented launches

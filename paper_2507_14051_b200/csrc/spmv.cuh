@@ -101,7 +101,7 @@ __device__ __forceinline__ void load_inputs(const Epi& epi, int64_t row,
                                             double (&ein)[Epi::NIN > 0 ? Epi::NIN : 1]) {
 #pragma unroll
   for (int k = 0; k < Epi::NIN; ++k) {
-    if constexpr (HasConstInputs<Epi>::value) {
+    if constexpr (RHP_CONST_INPUTS_KERNEL && HasConstInputs<Epi>::value) {
       ein[k] = (epi.cin.mask >> k) & 1u ? epi.cin.val[k] : epi.in[k][row];
     } else {
       ein[k] = epi.in[k][row];
@@ -324,12 +324,14 @@ __device__ __forceinline__ void warp_range(const int32_t* ci, const double* vals
 // the epilogue inputs, independent of the sum, are loaded first, so a row
 // costs one dependent chain (row pointers -> indices -> gathers) with its
 // epilogue loads in its shadow. WALK: epilogue only, same row -> thread map.
-template <class Epi, bool WALK, bool L1G = false>
+// RF rows in flight per thread: RHP_ROWS_IN_FLIGHT (2), RHP_UNIFORM_RF (1)
+// for uniform rows (no row-pointer round: one row's loads already fill the
+// memory pipe; C4 K2 612 -> 564 us, C3 22.9 -> 20.9 us; the walkers keep 2).
+template <class Epi, bool WALK, bool L1G = false, int RF = RHP_ROWS_IN_FLIGHT>
 __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* vals,
                                             const double* __restrict__ xg, const Sched& s,
                                             Epi& epi, double (&acc)[Epi::NRED]) {
   constexpr int NI = Epi::NIN > 0 ? Epi::NIN : 1;
-  constexpr int RF = RHP_ROWS_IN_FLIGHT;  // rows in flight per thread
   constexpr int EC = RF >= 4 ? 2 : 4;     // elements per row per step
   const int64_t G = static_cast<int64_t>(gridDim.x) * kBlock;
   const int64_t R = s.rows;
@@ -405,12 +407,30 @@ __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* val
   }
 }
 
+// The epilogue's block reductions and the last block's finalize.
+template <class Epi>
+__device__ __forceinline__ void spmv_tail(const Sched& s, Epi& epi, const double (&acc)[Epi::NRED],
+                                          double* part, unsigned int* ticket) {
+  if constexpr (Epi::REDUCE) {
+    block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
+    if constexpr (Epi::FINAL) {
+      if (elect_last_block(ticket)) {
+        epi.finalize(s, part, (int)gridDim.x);
+        if (threadIdx.x == 0) *ticket = 0u;
+      }
+    }
+  }
+}
+
 // L1G: L1-allocating gathers (ld_gather).
 // Epi provides: NRED (>= 1) reductions, NIN per-row input vectors `in[NIN]`,
 // REDUCE, FINAL; bool enter() (block-uniform early exit); void row(int64_t
 // i, double rowsum, const double* e, int stride, double(&acc)[NRED]) with
 // input k of row i at e[k*stride]; and, when FINAL, void finalize(const
 // Sched&, const double* part, int grid) (last block).
+// Merge-path operators launch this kernel, which holds only the merge path:
+// sharing one kernel with the thread-per-row variants cost C2's K2 4 us
+// (70.4 vs 66.4 us, A/B on one box).
 template <class Epi, bool L1G = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const double* __restrict__ xg,
                                                                  Sched s, Epi epi, double* part,
@@ -422,17 +442,38 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   double acc[Epi::NRED];
 #pragma unroll
   for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
-  if (s.thread_rows) thread_rows<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc);
-  else warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
-  if constexpr (Epi::REDUCE) {
-    block_reduce_store<Epi::NRED>(acc, part, gridDim.x, blockIdx.x);
-    if constexpr (Epi::FINAL) {
-      if (elect_last_block(ticket)) {
-        epi.finalize(s, part, (int)gridDim.x);
-        if (threadIdx.x == 0) *ticket = 0u;
-      }
-    }
-  }
+  warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
+  spmv_tail(s, epi, acc, part, ticket);
+}
+
+// Thread-per-row operators (Sched::thread_rows) launch this one; same grid
+// and epilogue contract as spmv_fused. It still carries the merge path
+// (RHP_ROWS_KERNEL_COMBINED, never taken at run time): the thread-per-row
+// code nvcc emits without it is slower (C4 K2 619 vs 565 us, C3 24.4 vs
+// 20.9 us, A/B on one box), and so is the rows-only kernel under a
+// shared-memory carveout preference (25-100 %: C4 K2 1.29 ms) — kept for
+// the measured speed.
+template <class Epi, bool L1G = false>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_rows(Csr A, const double* __restrict__ xg,
+                                                                Sched s, Epi epi, double* part,
+                                                                unsigned int* ticket) {
+  pdl_wait();
+  pdl_trigger();
+  if (!epi.enter()) return;
+  double acc[Epi::NRED];
+#pragma unroll
+  for (int q = 0; q < Epi::NRED; ++q) acc[q] = 0.0;
+#if RHP_ROWS_KERNEL_COMBINED
+  __shared__ __align__(16) WarpSmem wsm[kWarps];
+  if (!s.thread_rows) {
+    warp_range<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc, wsm[threadIdx.x >> 5]);
+  } else
+#endif
+  if (RHP_UNIFORM_ROWS && s.uniform_len > 0)
+    thread_rows<Epi, false, L1G, RHP_UNIFORM_RF>(A.ci, A.v, xg, s, epi, acc);
+  else
+    thread_rows<Epi, false, L1G>(A.ci, A.v, xg, s, epi, acc);
+  spmv_tail(s, epi, acc, part, ticket);
 }
 
 // Long-row engine (an operator made of few very long rows, e.g. C3's A:

@@ -65,6 +65,7 @@ class DeviceContext:
                 "sliced": {"A": bool(info.thread_rows & 8), "At": bool(info.thread_rows & 16)},
                 "uniform_rows": {"A": bool(info.thread_rows & 32),
                                  "At": bool(info.thread_rows & 64)},
+                "row_band": {"A": bool(info.thread_rows & 128), "At": bool(info.thread_rows & 256)},
                 "segments": {"A": info.segments & 0xffff, "At": info.segments >> 16},
                 "resident": bool(info.resident),
                 "const_bounds": [k for b, k in enumerate(("var_lb", "var_ub", "con_lb", "con_ub"))

@@ -514,6 +514,7 @@ class Session:
                 "cta_rows": {"A": bool(o[25] & 4)},
                 "sliced": {"A": bool(o[25] & 8), "At": bool(o[25] & 16)},
                 "uniform_rows": {"A": bool(o[25] & 32), "At": bool(o[25] & 64)},
+                "row_band": {"A": bool(o[25] & 128), "At": bool(o[25] & 256)},
                 "segments": {"A": int(o[26] & 0xffff), "At": int(o[26] >> 16)},
                 "resident": bool(o[27]),
                 "partition": {0: "single", 1: "replicated", 2: "sharded"}[int(o[28])],

@@ -512,3 +512,66 @@ def test_uniform_and_sliced_rows_are_bitwise_the_csr_path(gpu, case, monkeypatch
         r = got[mode, "solve"]
         assert r.iterations == base.iterations, mode
         assert np.array_equal(r.x, base.x) and np.array_equal(r.y, base.y), mode
+
+
+def row_band_lp():
+    """Rows [1000, 2500) of length 12 whose column advances with the row at
+    every element position (row 1000 + r holds columns t * 1500 + r, the
+    shape of C4's arc-capacity rows), between ragged random rows (1..20)."""
+    rng = np.random.default_rng(11)
+    m, n, B = 3000, 18000, 1500
+    rows = []
+    for i in range(m):
+        if 1000 <= i < 2500:
+            rows.append(np.arange(12) * B + (i - 1000))
+        else:
+            rows.append(np.sort(rng.choice(n, rng.integers(1, 21), replace=False)))
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])])
+    ci = np.concatenate(rows)
+    v = rng.uniform(0.5, 2.0, len(ci)) * rng.choice([-1.0, 1.0], len(ci))
+    return LpProblem(m, n, rp, ci, v, rng.uniform(-1, 1, n), [-1.0] * n, [1.0] * n,
+                     [-5.0] * m, [5.0] * m)
+
+
+@pytest.mark.parametrize("colsegs", [False, True], ids=["plain", "with_column_segments"])
+def test_row_band_matches_oracle(gpu, colsegs, monkeypatch):
+    """A thread-per-row row band carved out of a merge-path operator
+    (rhp_cuda.cu carve_row_band; forced here, the LP is below the size
+    thresholds), alone and next to column segments of another row band:
+    SpMVs within 1e-13 of the oracle, first iterates within 1e-10, the
+    solve's objective within 1e-6 and the oracle's KKT check at eps."""
+    lp = row_band_lp()
+    monkeypatch.setenv("RHP_ROW_BAND", "force")
+    if colsegs:  # 1 KB column segments over rows [0, 1000)
+        monkeypatch.setenv("RHP_SEG_BYTES", "1024")
+        monkeypatch.setenv("RHP_SEG_FORCE", "1")
+        monkeypatch.setenv("RHP_SEG_BAND", "0,1000")
+    rng = np.random.default_rng(9)
+    x, y = rng.uniform(-1, 1, lp.num_vars), rng.uniform(-1, 1, lp.num_cons)
+    O = support.oracle()
+    with DeviceContext(lp) as dev:
+        dev.scale(enabled=False)
+        lay = dev.layout()
+        ax, aty = dev.spmv(x), dev.spmv(y, True)
+    assert lay["row_band"]["A"] and not lay["row_band"]["At"]
+    col_segs = -(-lp.num_vars * 8 // 1024) if colsegs else 1
+    assert lay["segments"]["A"] == col_segs + 1
+    assert max_rel(ax, support.spmv_with(O, lp, x)) <= 1e-13
+    assert max_rel(aty, support.spmv_with(O, lp, y, True)) <= 1e-13
+    from paper_2507_14051_b200.lp import set_resident
+
+    k = 100
+    cfg = SolverConfig(epsilon=1e-7)
+    try:
+        set_resident(0)  # the segmented multi-CTA engines
+        g = solve(lp, SolverConfig(epsilon=1e-300, iteration_limit=k))
+        o = support.solve_with(O, lp, SolverConfig(epsilon=1e-300, iteration_limit=k))
+        assert max_rel(g.x, o.x) <= 1e-10 and max_rel(g.y, o.y) <= 1e-10
+        g = solve(lp, cfg)
+    finally:
+        set_resident(-1)
+    o = support.solve_with(O, lp, cfg)
+    assert g.status == o.status == "optimal"
+    assert abs(g.objective - o.objective) <= 1e-6 * max(1.0, abs(o.objective))
+    r = support.kkt_with(O, lp, g.x, g.y)
+    assert r["gap_rel"] <= 1e-7 and r["primal_rel"] <= 1e-7

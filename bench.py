@@ -484,15 +484,16 @@ def run_product(args):
         t = json.loads(tf.read_text()).get(args.config)
         if t and dist.world == 1:
             traffic = t.get(dominant)
+    dom_rows = bool(layout.get("thread_rows", {}).get("At" if dominant == "k2" else "A"))
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": "profiles/ncu_traffic.json (ncu dram read+write per launch)"
                 if traffic else None,
-                "kernel": ("spmv_fused<EpiAty> (A^T y+ + aty Halpern + next primal step)"
-                           if dominant == "k2" else
-                           "spmv_fused<EpiDual> (A x+ + dual step + Halpern/reflection)")
-                + (" [thread-per-row engine]" if layout.get("thread_rows", {}).get(
-                    "At" if dominant == "k2" else "A") else " [merge-path engine]"),
+                "kernel": (("spmv_rows" if dom_rows else "spmv_fused")
+                           + ("<EpiAty> (A^T y+ + aty Halpern + next primal step)"
+                              if dominant == "k2" else
+                              "<EpiDual> (A x+ + dual step + Halpern/reflection)"))
+                + (" [thread-per-row engine]" if dom_rows else " [merge-path engine]"),
                 "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "bytes_per_launch": k2b if dominant == "k2" else k1b,
                 "kernels": {"k1_ms": kt["k1_dual_spmv_ms"], "k1_gbs": k1,

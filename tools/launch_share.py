@@ -10,7 +10,7 @@ import re
 
 
 def short(name):
-    m = re.search(r"(spmv_fused|epilogue_walk|k_\w+)<(?:rhp::)?(\w+)>", name)
+    m = re.search(r"(spmv_fused|spmv_rows|spmv_cta_rows|epilogue_walk|k_\w+)<(?:rhp::)?(\w+)>", name)
     if m:
         return f"{m.group(1)}<{m.group(2)}>"
     return name.split("(")[0].replace("void ", "").replace("rhp::", "")

@@ -19,6 +19,7 @@ struct DeviceOptions {
   bool use_graph = true;   // CUDA graph with a conditional WHILE node per block
   long block_limit = 64;   // PDHG iterations per device block at most
   int resident = -1;       // small LPs: one cluster runs whole blocks (-1 auto, 0 off, 1 on)
+  int locality = 0;        // first-touch row/column relabelling (0 auto, -1 off, 1 forced)
   // Row-partitioned multi-GPU solve (one process per GPU): every rank calls
   // solve() on the FULL problem with the same config; rank 0's 128-byte
   // ncclUniqueId (rhp_nccl_unique_id) is shared out of band. An id with

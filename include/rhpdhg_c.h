@@ -184,6 +184,11 @@ int rhpdhg_run_benchmark(const char* dir, const rhpdhg_config_c* cfg, double sma
                          char* table, int64_t table_cap);
 /* Small-LP cluster-resident device blocks: -1 auto (default), 0 off, 1 on. */
 int rhpdhg_set_resident(int mode);
+/* First-touch locality relabelling of rows and columns at device ingest (the
+ * calling thread's solves): 0 auto (default: large gathered vectors, kept
+ * only when it cuts the SpMV gather sectors), -1 off, 1 forced. Results come
+ * back in the original order either way. */
+int rhpdhg_set_locality(int mode);
 
 /* Resumable solve (extension used by benchmarks and long-running callers):
  * create = validation + upload + scaling + power iteration + initial KKT

@@ -58,7 +58,11 @@ typedef struct rhp_options {
   int64_t block_limit;   /* max PDHG iterations per device block (default 64) */
   const void* nccl_id;   /* 128 bytes when world_size > 1, else NULL */
   int32_t resident;      /* small-LP cluster-resident blocks: -1 auto, 0 off, 1 on */
-  int32_t pad_;
+  /* locality relabelling of rows and columns at ingest (ingest.cu
+   * maybe_relabel): 0 auto (large gathered vectors, kept when it cuts the
+   * gather sectors), < 0 off, > 0 forced; single-GPU contexts only. The
+   * RHP_LOCALITY environment variable overrides it. */
+  int32_t locality;
   /* In-process collective group (rhp_local_group_create) instead of NCCL:
    * world_size contexts of ONE process, each driven by its own host thread,
    * exchange through device memory with rank-ordered reductions. Lets the
@@ -152,6 +156,10 @@ typedef struct rhp_layout_info {
                            (Option A: allreduce / peer exchange), 2 sharded (Option B) */
   int32_t const_bounds; /* bounds constant after scaling, taken from kernel parameters instead of
                            loaded: bit 0 var_lb, 1 var_ub, 2 con_lb, 3 con_ub */
+  int32_t relabel;      /* rows and columns renumbered in first-touch locality order */
+  int32_t pad2_;
+  double sectors[4];    /* gather sectors per nonzero (256-nonzero windows): A, A^T as given,
+                           A, A^T relabelled (0 when not evaluated) */
 } rhp_layout_info;
 
 const char* rhp_last_error(void);

@@ -121,7 +121,7 @@ class RhpOptions(C.Structure):
         ("block_limit", C.c_int64),
         ("nccl_id", C.c_void_p),
         ("resident", C.c_int32),
-        ("pad_", C.c_int32),
+        ("locality", C.c_int32),
         ("local_group", C.c_void_p),
     ]
 
@@ -181,6 +181,7 @@ class RhpLayoutInfo(C.Structure):
         ("sm_count", C.c_int32), ("gather_l1", C.c_int32), ("pdl", C.c_int32),
         ("thread_rows", C.c_int32), ("segments", C.c_int32),
         ("resident", C.c_int32), ("partition", C.c_int32), ("const_bounds", C.c_int32),
+        ("relabel", C.c_int32), ("pad2_", C.c_int32), ("sectors", C.c_double * 4),
     ]
 
 
@@ -200,7 +201,7 @@ CUDA_SYMBOLS = [
 HOST_SYMBOLS = [
     "rhpdhg_config_default", "rhpdhg_solve_csr", "rhpdhg_kkt_residuals", "rhpdhg_last_error",
     "rhpdhg_set_device", "rhpdhg_set_device_options", "rhpdhg_set_distributed",
-    "rhpdhg_set_resident", "rhpdhg_set_local_group", "rhpdhg_run_benchmark",
+    "rhpdhg_set_resident", "rhpdhg_set_locality", "rhpdhg_set_local_group", "rhpdhg_run_benchmark",
     "rhpdhg_session_create",
     "rhpdhg_session_advance", "rhpdhg_session_info", "rhpdhg_session_timer",
     "rhpdhg_session_finish", "rhpdhg_session_destroy", "rhpdhg_session_time_kernels",
@@ -301,6 +302,7 @@ def load_host() -> C.CDLL:
             "rhpdhg_run_benchmark": [C.c_char_p, C.POINTER(ConfigC), C.c_double, C.c_double,
                                      C.c_int, C.c_char_p, C.c_char_p, C.c_int64],
             "rhpdhg_set_resident": [C.c_int],
+            "rhpdhg_set_locality": [C.c_int],
             "rhpdhg_session_create": [C.POINTER(LpView), C.POINTER(ConfigC), C.POINTER(P)],
             "rhpdhg_session_advance": [P, C.c_int64, C.POINTER(C.c_int32)],
             "rhpdhg_session_info": [P, c_int64_p, c_int64_p, C.POINTER(KktC), c_double_p,

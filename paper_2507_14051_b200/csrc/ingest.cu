@@ -17,11 +17,13 @@
 //     exclusive scan, then a gather of row ids and values.
 // Only the row pointers (O(m + n)) come back to the host, for the warp
 // schedules. C4 (60M nonzeros): host layout 2.6 s -> device ingest ≈ 0.2 s.
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -137,10 +139,251 @@ int end_bit_for(int64_t n) {
   return b;
 }
 
+
+// A^T (arrays allocated, rows = n) from A: stable radix sort of the element
+// positions keyed by column, so rows stay ascending inside every column.
+void build_transpose(const DeviceCsr& A, int64_t n, DeviceCsr& At, cudaStream_t s) {
+  const int64_t nnz = A.nnz, m = A.rows;
+  ICK(cudaMemsetAsync(At.rp, 0, (n + 1) * sizeof(int64_t), s));
+  if (!nnz) return;
+  Scratch<int32_t> keys_out(nnz), idx_in(nnz), idx_out(nnz);
+  k_iota<<<blocks_for(nnz), kThreads, 0, s>>>(idx_in.p, nnz);
+  size_t tb = 0;
+  const int eb = end_bit_for(n);
+  ICK(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.ci, keys_out.p, idx_in.p, idx_out.p, nnz, 0, eb, s));
+  Scratch<unsigned char> tmp(tb);
+  ICK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, A.ci, keys_out.p, idx_in.p, idx_out.p, nnz, 0, eb, s));
+  Scratch<int64_t> cnt(n + 1);
+  ICK(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int64_t), s));
+  k_col_hist<<<blocks_for(nnz), kThreads, 0, s>>>(A.ci, nnz, cnt.p);
+  size_t tb2 = 0;
+  ICK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt.p, At.rp, n + 1, s));
+  Scratch<unsigned char> tmp2(tb2);
+  ICK(cub::DeviceScan::ExclusiveSum(tmp2.p, tb2, cnt.p, At.rp, n + 1, s));
+  k_gather_t<<<blocks_for(nnz), kThreads, 0, s>>>(idx_out.p, A.rp, m, A.v, nnz, At.ci, At.v);
+  ICK(cudaGetLastError());
+  ICK(cudaStreamSynchronize(s));
+}
+
+// ---- locality relabelling ------------------------------------------------
+//
+// The SpMV gathers x[c] (A) and y[r] (A^T) one 8-B element per nonzero; what
+// the gathers cost is the number of distinct 32-B sectors a warp's window
+// touches (L1TEX / L2 sector throughput, not HBM bytes). When
+// the gathered vectors are larger than L2's comfortable share, rows and
+// columns are renumbered in first-touch order — columns by the first row that
+// uses them, then rows by the first (renumbered) column they use, twice —
+// so the columns of neighbouring rows sit in neighbouring sectors (C4's
+// arcs of one node, its commodity rows next to its capacity rows). The
+// relabelling is kept only if the measured sectors per window drop by
+// kRelabelGain; the device order maps (HostLayout::prow / pcol) carry it to
+// every host<->device copy, so nothing outside the device sees it. The
+// arithmetic is unchanged; only summation orders move (tolerance-level, like
+// any reduction order).
+
+constexpr double kRelabelGain = 0.8;  // keep when sectors(new) <= 0.8 * sectors(old)
+constexpr int kRelabelPasses = 2;
+
+// key[j] = first row touching column j (A^T rows ascend), empty: UINT32_MAX
+__global__ void k_col_first(const int64_t* trp, const int32_t* tci, int64_t n, uint32_t* key) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    key[j] = trp[j + 1] > trp[j] ? static_cast<uint32_t>(tci[trp[j]]) : 0xFFFFFFFFu;
+}
+
+// key[i] = smallest new label among row i's columns, empty: UINT32_MAX
+__global__ void k_row_first(const int64_t* rp, const int32_t* ci, int64_t m, const int32_t* clab,
+                            uint32_t* key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t k = 0xFFFFFFFFu;
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) k = min(k, static_cast<uint32_t>(clab[ci[e]]));
+    key[i] = k;
+  }
+}
+
+// lab[order[i]] = i
+__global__ void k_invert(const int32_t* order, int64_t n, int32_t* lab) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lab[order[i]] = static_cast<int32_t>(i);
+}
+
+// out[i] = in[order[i]] (composition of order maps)
+__global__ void k_compose(const int32_t* in, const int32_t* order, int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[order[i]];
+}
+
+// element keys (new row << 32 | new column) of A, one thread per row
+__global__ void k_elem_keys(const int64_t* rp, const int32_t* ci, int64_t m, const int32_t* rlab,
+                            const int32_t* clab, uint64_t* key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t hi = static_cast<uint64_t>(static_cast<uint32_t>(rlab[i])) << 32;
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e)
+      key[e] = hi | static_cast<uint32_t>(clab[ci[e]]);
+  }
+}
+
+__global__ void k_split_keys(const uint64_t* key, int64_t nz, int32_t* ci, int64_t* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    ci[e] = static_cast<int32_t>(key[e] & 0xFFFFFFFFull);
+    atomicAdd(reinterpret_cast<unsigned long long*>(cnt + (key[e] >> 32)), 1ull);
+  }
+}
+
+// distinct 32-B sectors of the gathered vector per window of 256 consecutive
+// nonzeros (one window per CTA pass: block radix sort + adjacent difference)
+__global__ void __launch_bounds__(256) k_window_sectors(const int32_t* ci, int64_t nz,
+                                                        unsigned long long* total) {
+  using Sort = cub::BlockRadixSort<uint32_t, 256, 1>;
+  __shared__ typename Sort::TempStorage ts;
+  __shared__ uint32_t sorted[256];
+  unsigned long long mine = 0;
+  for (int64_t w = blockIdx.x; w * 256 < nz; w += gridDim.x) {
+    const int64_t e = w * 256 + threadIdx.x;
+    uint32_t k[1] = {e < nz ? static_cast<uint32_t>(ci[e]) >> 2 : 0xFFFFFFFFu};
+    Sort(ts).Sort(k);
+    sorted[threadIdx.x] = k[0];
+    __syncthreads();
+    const bool fresh = k[0] != 0xFFFFFFFFu && (threadIdx.x == 0 || sorted[threadIdx.x - 1] != k[0]);
+    const int cnt = __syncthreads_count(fresh);
+    if (threadIdx.x == 0) mine += static_cast<unsigned long long>(cnt);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && mine) atomicAdd(total, mine);
+}
+
+unsigned long long window_sectors(const DeviceCsr& op, cudaStream_t s) {
+  if (!op.nnz) return 0;
+  Scratch<unsigned long long> t(1);
+  ICK(cudaMemsetAsync(t.p, 0, sizeof(unsigned long long), s));
+  const int64_t wins = (op.nnz + 255) / 256;
+  k_window_sectors<<<static_cast<unsigned>(std::min<int64_t>(wins, 148 * 16)), 256, 0, s>>>(op.ci, op.nnz, t.p);
+  ICK(cudaGetLastError());
+  unsigned long long h = 0;
+  ICK(cudaMemcpyAsync(&h, t.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  ICK(cudaStreamSynchronize(s));
+  return h;
+}
+
+// order[i] = the index with the i-th smallest key (ties by index: stable)
+void order_by_key(const uint32_t* key, int64_t n, int32_t* order, cudaStream_t s) {
+  Scratch<uint32_t> kout(n);
+  Scratch<int32_t> idx(n);
+  k_iota<<<blocks_for(n), kThreads, 0, s>>>(idx.p, n);
+  size_t tb = 0;
+  ICK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, kout.p, idx.p, order, n, 0, 32, s));
+  Scratch<unsigned char> tmp(tb);
+  ICK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key, kout.p, idx.p, order, n, 0, 32, s));
+}
+
+// One first-touch pass: new column order from A^T, new row order from the
+// renumbered columns, then A rebuilt (rows by new label, columns ascending
+// by new label) and A^T from it. order_r / order_c (device) compose: entry
+// i = the ORIGINAL index now at position i.
+void relabel_pass(DeviceCsr& A, DeviceCsr& At, int64_t m, int64_t n, int32_t* order_r, int32_t* order_c,
+                  cudaStream_t s) {
+  const int64_t nnz = A.nnz;
+  Scratch<uint32_t> ckey(n), rkey(m);
+  Scratch<int32_t> cord(n), clab(n), rord(m), rlab(m), tmp_r(m), tmp_c(n);
+  k_col_first<<<blocks_for(n), kThreads, 0, s>>>(At.rp, At.ci, n, ckey.p);
+  order_by_key(ckey.p, n, cord.p, s);
+  k_invert<<<blocks_for(n), kThreads, 0, s>>>(cord.p, n, clab.p);
+  k_row_first<<<blocks_for(m), kThreads, 0, s>>>(A.rp, A.ci, m, clab.p, rkey.p);
+  order_by_key(rkey.p, m, rord.p, s);
+  k_invert<<<blocks_for(m), kThreads, 0, s>>>(rord.p, m, rlab.p);
+  {
+    Scratch<uint64_t> kin(nnz), kout(nnz);
+    Scratch<double> vout(nnz);
+    k_elem_keys<<<blocks_for(m), kThreads, 0, s>>>(A.rp, A.ci, m, rlab.p, clab.p, kin.p);
+    size_t tb = 0;
+    const int eb = 32 + end_bit_for(m);
+    ICK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.p, kout.p, A.v, vout.p, nnz, 0, eb, s));
+    Scratch<unsigned char> tmp(tb);
+    ICK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kin.p, kout.p, A.v, vout.p, nnz, 0, eb, s));
+    Scratch<int64_t> cnt(m + 1);
+    ICK(cudaMemsetAsync(cnt.p, 0, (m + 1) * sizeof(int64_t), s));
+    k_split_keys<<<blocks_for(nnz), kThreads, 0, s>>>(kout.p, nnz, A.ci, cnt.p);
+    size_t tb2 = 0;
+    ICK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt.p, A.rp, m + 1, s));
+    Scratch<unsigned char> tmp2(tb2);
+    ICK(cub::DeviceScan::ExclusiveSum(tmp2.p, tb2, cnt.p, A.rp, m + 1, s));
+    ICK(cudaMemcpyAsync(A.v, vout.p, nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    ICK(cudaGetLastError());
+    ICK(cudaStreamSynchronize(s));
+  }
+  build_transpose(A, n, At, s);
+  k_compose<<<blocks_for(m), kThreads, 0, s>>>(order_r, rord.p, m, tmp_r.p);
+  k_compose<<<blocks_for(n), kThreads, 0, s>>>(order_c, cord.p, n, tmp_c.p);
+  ICK(cudaMemcpyAsync(order_r, tmp_r.p, m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  ICK(cudaMemcpyAsync(order_c, tmp_c.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  ICK(cudaGetLastError());
+  ICK(cudaStreamSynchronize(s));
+}
+
+// locality: 0 auto (gathered vector > kGatherL2Bytes / 4 and fewer sectors),
+// < 0 off, > 0 forced (tests). Returns whether the layout was relabelled;
+// order_r / order_c (host) then hold the original index at each position.
+bool maybe_relabel(DeviceCsr& A, DeviceCsr& At, int64_t m, int64_t n, int locality,
+                   std::vector<int32_t>& order_r, std::vector<int32_t>& order_c, double (&sectors)[4],
+                   cudaStream_t s) {
+  for (double& x : sectors) x = 0.0;
+  if (locality < 0 || A.nnz == 0 || m == 0 || n == 0) return false;
+  const double big = kGatherL2Bytes / 4.0;
+  if (locality == 0 && !(8.0 * static_cast<double>(n) > big || 8.0 * static_cast<double>(m) > big))
+    return false;
+  const double sa0 = static_cast<double>(window_sectors(A, s)), st0 = static_cast<double>(window_sectors(At, s));
+  const double before = sa0 + st0;
+  sectors[0] = sa0 / static_cast<double>(A.nnz);
+  sectors[1] = st0 / static_cast<double>(A.nnz);
+  // keep A's original arrays until the verdict (A^T is rebuilt from them on
+  // a revert); skipped in auto mode when the device cannot hold the copies
+  // and the sort buffers (~60 B per nonzero)
+  const int64_t nnz = A.nnz;
+  if (locality == 0) {
+    size_t free_b = 0, total_b = 0;
+    ICK(cudaMemGetInfo(&free_b, &total_b));
+    if (static_cast<double>(free_b) < 1.25 * 60.0 * static_cast<double>(nnz) + 1e9) return false;
+  }
+  Scratch<int64_t> a_rp(m + 1);
+  Scratch<int32_t> a_ci(nnz);
+  Scratch<double> a_v(nnz);
+  ICK(cudaMemcpyAsync(a_rp.p, A.rp, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  ICK(cudaMemcpyAsync(a_ci.p, A.ci, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  ICK(cudaMemcpyAsync(a_v.p, A.v, nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  Scratch<int32_t> ordr(m), ordc(n);
+  k_iota<<<blocks_for(m), kThreads, 0, s>>>(ordr.p, m);
+  k_iota<<<blocks_for(n), kThreads, 0, s>>>(ordc.p, n);
+  ICK(cudaGetLastError());
+  int passes = kRelabelPasses;
+  if (const char* e = std::getenv("RHP_RELABEL_PASSES")) passes = std::max(1, std::atoi(e));
+  for (int p = 0; p < passes; ++p) relabel_pass(A, At, m, n, ordr.p, ordc.p, s);
+  const double sa = static_cast<double>(window_sectors(A, s)), st = static_cast<double>(window_sectors(At, s));
+  sectors[2] = sa / static_cast<double>(nnz);
+  sectors[3] = st / static_cast<double>(nnz);
+  if (locality == 0 && sa + st > kRelabelGain * before) {  // not worth it: restore
+    ICK(cudaMemcpyAsync(A.rp, a_rp.p, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    ICK(cudaMemcpyAsync(A.ci, a_ci.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    ICK(cudaMemcpyAsync(A.v, a_v.p, nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    build_transpose(A, n, At, s);
+    return false;
+  }
+  order_r.resize(static_cast<size_t>(m));
+  order_c.resize(static_cast<size_t>(n));
+  ICK(cudaMemcpyAsync(order_r.data(), ordr.p, m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  ICK(cudaMemcpyAsync(order_c.data(), ordc.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  ICK(cudaStreamSynchronize(s));
+  return true;
+}
+
 }  // namespace
 
 void ingest_device(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end, HostLayout& L,
-                   DeviceCsr& A, DeviceCsr& At, cudaStream_t s) {
+                   DeviceCsr& A, DeviceCsr& At, int locality, cudaStream_t s) {
   const int64_t n = lp.num_vars;
   if (n > INT32_MAX || lp.num_cons > INT32_MAX)
     throw std::invalid_argument("device layout supports at most 2^31-1 rows and columns");
@@ -231,25 +474,12 @@ void ingest_device(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end,
   At.rp = dev_alloc_zero<int64_t>(n + 1);
   At.ci = dev_alloc_zero<int32_t>(nnz);
   At.v = dev_alloc_zero<double>(nnz);
-  if (nnz) {
-    Scratch<int32_t> keys_out(nnz), idx_in(nnz), idx_out(nnz);
-    k_iota<<<blocks_for(nnz), kThreads, 0, s>>>(idx_in.p, nnz);
-    size_t tb = 0;
-    const int eb = end_bit_for(n);
-    ICK(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.ci, keys_out.p, idx_in.p, idx_out.p, nnz, 0, eb, s));
-    Scratch<unsigned char> tmp(tb);
-    ICK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, A.ci, keys_out.p, idx_in.p, idx_out.p, nnz, 0, eb, s));
-    Scratch<int64_t> cnt(n + 1);
-    ICK(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int64_t), s));
-    k_col_hist<<<blocks_for(nnz), kThreads, 0, s>>>(A.ci, nnz, cnt.p);
-    size_t tb2 = 0;
-    ICK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt.p, At.rp, n + 1, s));
-    Scratch<unsigned char> tmp2(tb2);
-    ICK(cub::DeviceScan::ExclusiveSum(tmp2.p, tb2, cnt.p, At.rp, n + 1, s));
-    k_gather_t<<<blocks_for(nnz), kThreads, 0, s>>>(idx_out.p, A.rp, m, A.v, nnz, At.ci, At.v);
-    ICK(cudaGetLastError());
-    ICK(cudaStreamSynchronize(s));
-  }
+  build_transpose(A, n, At, s);
+
+  // (4b) locality relabelling of rows and columns (large gathered vectors)
+  std::vector<int32_t> order_r, order_c;
+  L.relabel = maybe_relabel(A, At, m, n, locality, order_r, order_c, L.sectors, s);
+
   A.v_orig = dev_alloc_zero<double>(nnz);
   At.v_orig = dev_alloc_zero<double>(nnz);
   if (nnz) {
@@ -272,11 +502,12 @@ void ingest_device(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end,
   ICK(cudaMemcpyAsync(ht.rp.data(), At.rp, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   ICK(cudaStreamSynchronize(s));
 
-  // (6) identity order maps (rows and columns keep the original order)
+  // (6) order maps: device row / column -> original (identity unless relabelled)
   L.prow.resize(static_cast<size_t>(m));
-  for (int64_t r = 0; r < m; ++r) L.prow[r] = static_cast<int32_t>(row_begin + r);
+  for (int64_t r = 0; r < m; ++r)
+    L.prow[r] = static_cast<int32_t>(row_begin + (L.relabel ? order_r[r] : r));
   L.pcol.resize(static_cast<size_t>(n));
-  for (int64_t j = 0; j < n; ++j) L.pcol[j] = static_cast<int32_t>(j);
+  for (int64_t j = 0; j < n; ++j) L.pcol[j] = L.relabel ? order_c[j] : static_cast<int32_t>(j);
 }
 
 }  // namespace rhp

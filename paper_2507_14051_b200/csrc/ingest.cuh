@@ -49,8 +49,10 @@ T* dev_alloc_zero(size_t count) {
 // operators (A: local rows x n, A^T: n x local rows) and the host row
 // pointers / order maps of L. Throws std::out_of_range (column out of
 // range), std::domain_error (non-finite value, duplicate/unsorted entry),
-// std::invalid_argument (too large), DeviceFailure.
+// std::invalid_argument (too large), DeviceFailure. locality (rhp_options):
+// 0 auto / < 0 off / > 0 forced first-touch relabelling of rows and columns
+// (ingest.cu maybe_relabel; L.prow / L.pcol carry it).
 void ingest_device(const rhpdhg_lp_view& lp, int64_t row_begin, int64_t row_end, HostLayout& L,
-                   DeviceCsr& A, DeviceCsr& At, cudaStream_t s);
+                   DeviceCsr& A, DeviceCsr& At, int locality, cudaStream_t s);
 
 }  // namespace rhp

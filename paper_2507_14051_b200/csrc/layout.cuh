@@ -56,6 +56,8 @@ struct HostLayout {
   int64_t nnz = 0;                     // local nonzeros (explicit zeros dropped)
   std::vector<int32_t> prow;           // device row -> original row (global index)
   std::vector<int32_t> pcol;           // device col -> original col
+  bool relabel = false;                // first-touch locality order (ingest.cu)
+  double sectors[4] = {0, 0, 0, 0};    // gather sectors / nnz: A, A^T before, after
   HostOperator A, At;
 };
 

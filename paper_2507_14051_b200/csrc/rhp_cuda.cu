@@ -903,8 +903,9 @@ void build_segments(rhp_ctx& c, DevOp& d, const HostOperator& h, int64_t cols, i
 // 22.9k both, C4 1102 vs 1076 iter/s), so the policy is fixed and
 // deterministic. The policy never changes a result.
 void choose_gather_policy(rhp_ctx& c) {
-  const char* env = std::getenv("RHP_L1_GATHER");
-  c.A.l1g = c.At.l1g = env && env[0] == '1';
+  const char* env = std::getenv("RHP_L1_GATHER");  // 1: both operators, A / T: one of them
+  c.A.l1g = env && (env[0] == '1' || env[0] == 'A');
+  c.At.l1g = env && (env[0] == '1' || env[0] == 'T');
 }
 
 // Peer-memory exchange (peer.cuh): one cudaMalloc'd region per rank, its
@@ -1488,10 +1489,12 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
       c->offsets = partition_rows(*lp, c->world);
       for (int r = 0; r < c->world; ++r)
         c->max_local = std::max(c->max_local, c->offsets[r + 1] - c->offsets[r]);
-      ingest_device(*lp, c->offsets[c->rank], c->offsets[c->rank + 1], c->L, c->A, c->At, c->stream);
+      ingest_device(*lp, c->offsets[c->rank], c->offsets[c->rank + 1], c->L, c->A, c->At, -1, c->stream);
     } else {
       phase("device init");
-      ingest_device(*lp, 0, lp->num_cons, c->L, c->A, c->At, c->stream);
+      int locality = opt.locality;
+      if (const char* e = std::getenv("RHP_LOCALITY")) locality = std::atoi(e);
+      ingest_device(*lp, 0, lp->num_cons, c->L, c->A, c->At, locality, c->stream);
     }
     phase("ingest");
     const HostLayout& L = c->L;
@@ -1680,6 +1683,8 @@ int rhp_layout(rhp_ctx* c, rhp_layout_info* info) {
     info->resident = c->resident ? 1 : 0;
     info->partition = !c->dist ? 0 : c->sharded ? 2 : 1;
     info->const_bounds = static_cast<int32_t>(c->const_mask);
+    info->relabel = c->L.relabel ? 1 : 0;
+    for (int k = 0; k < 4; ++k) info->sectors[k] = c->L.sectors[k];
     info->segments = static_cast<int32_t>(std::max<size_t>(1, c->A.segs.size()) |
                                           (std::max<size_t>(1, c->At.segs.size()) << 16));
   });

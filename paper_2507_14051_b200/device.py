@@ -18,11 +18,12 @@ def _p(a):
 
 class DeviceContext:
     def __init__(self, lp: LpProblem, device: int = 0, use_graph: bool = True,
-                 block_limit: int = 64, resident: int = 0):
+                 block_limit: int = 64, resident: int = 0, locality: int = -1):
         self.lib = capi.load_cuda()
         self.lp = lp
         opt = capi.RhpOptions(device=device, rank=0, world_size=1, use_graph=int(use_graph),
-                              block_limit=block_limit, nccl_id=None, resident=resident)
+                              block_limit=block_limit, nccl_id=None, resident=resident,
+                              locality=locality)
         h = C.c_void_p()
         self._view = lp.view()
         self._ok(self.lib.rhp_create(C.byref(self._view), C.byref(opt), C.byref(h)))
@@ -69,7 +70,8 @@ class DeviceContext:
                 "segments": {"A": info.segments & 0xffff, "At": info.segments >> 16},
                 "resident": bool(info.resident),
                 "const_bounds": [k for b, k in enumerate(("var_lb", "var_ub", "con_lb", "con_ub"))
-                                 if (info.const_bounds >> b) & 1]}
+                                 if (info.const_bounds >> b) & 1],
+                "relabel": bool(info.relabel), "sectors": list(info.sectors)}
 
     def scale(self, enabled=True, ruiz=10, pock_chambolle=True):
         self._ok(self.lib.rhp_scale(self.h, int(enabled), ruiz, int(pock_chambolle)))

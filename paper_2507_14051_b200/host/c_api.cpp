@@ -186,6 +186,10 @@ int rhpdhg_set_resident(int mode) {
   return guarded([&] { default_device_options().resident = mode < 0 ? -1 : (mode ? 1 : 0); });
 }
 
+int rhpdhg_set_locality(int mode) {
+  return guarded([&] { default_device_options().locality = mode < 0 ? -1 : (mode ? 1 : 0); });
+}
+
 int rhpdhg_set_distributed(int rank, int world_size, const void* nccl_id) {
   return guarded([&] {
     if (world_size < 1 || rank < 0 || rank >= world_size) throw UsageError("bad rank/world_size");
@@ -301,6 +305,8 @@ int rhpdhg_session_layout(rhpdhg_session* s, int64_t* o) {
     o[27] = li.resident;
     o[28] = li.partition;
     o[29] = li.const_bounds;
+    o[30] = li.relabel;
+    for (int k = 0; k < 4; ++k) std::memcpy(&o[31 + k], &li.sectors[k], sizeof(double));
   });
 }
 

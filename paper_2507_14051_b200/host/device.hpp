@@ -71,6 +71,7 @@ inline rhp_options options(int device, bool use_graph, long block_limit) {
   o.nccl_id = nullptr;
   o.local_group = nullptr;
   o.resident = 0;  // per-op contexts (products, KKT, scaling) never use resident blocks
+  o.locality = -1;  // nor a relabelled layout (CSC values keep the reference's element order)
   return o;
 }
 
@@ -80,6 +81,7 @@ template <class DeviceOptionsT>
 inline rhp_options options(const DeviceOptionsT& d) {
   rhp_options o = options(d.device, d.use_graph, d.block_limit);
   o.resident = d.resident;
+  o.locality = d.locality;
   o.rank = d.rank;
   o.world_size = d.world_size;
   if (!d.nccl_id.empty()) {

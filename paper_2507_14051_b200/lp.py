@@ -394,6 +394,12 @@ def set_resident(mode: int = -1) -> None:
     raise_status(lib.rhpdhg_set_resident(mode), lib.rhpdhg_last_error().decode())
 
 
+def set_locality(mode: int = 0) -> None:
+    """First-touch row/column relabelling at device ingest: 0 auto, -1 off, 1 forced."""
+    lib = capi.load_host()
+    raise_status(lib.rhpdhg_set_locality(mode), lib.rhpdhg_last_error().decode())
+
+
 def nccl_unique_id() -> bytes:
     """rank 0: a fresh 128-byte ncclUniqueId to share with the other ranks."""
     lib = capi.load_cuda()
@@ -504,7 +510,7 @@ class Session:
         return {"A": ms[0], "At": ms[1]}
 
     def layout(self) -> dict:
-        o = (C.c_int64 * 30)()
+        o = (C.c_int64 * 35)()
         self._check(self._lib.rhpdhg_session_layout(self._h, o))
         return {"m": o[0], "n": o[1], "nnz": o[2], "row_bins": list(o[3:11]),
                 "col_bins": list(o[11:19]), "grid_a": o[19], "grid_at": o[20],
@@ -519,7 +525,10 @@ class Session:
                 "resident": bool(o[27]),
                 "partition": {0: "single", 1: "replicated", 2: "sharded"}[int(o[28])],
                 "const_bounds": [k for b, k in enumerate(("var_lb", "var_ub", "con_lb", "con_ub"))
-                                 if (o[29] >> b) & 1]}
+                                 if (o[29] >> b) & 1],
+                "relabel": bool(o[30]),
+                "gather_sectors_per_nnz": [C.cast(C.pointer(C.c_int64(o[31 + k])),
+                                                  C.POINTER(C.c_double))[0] for k in range(4)]}
 
     def finish(self) -> SolutionReport:
         def fn(view, cc, rep, x, y, rc_, hist, cap):

@@ -38,6 +38,15 @@ constexpr int kWarps = kBlock / 32;
 #define RHP_MIN_BLOCKS 2
 #endif
 constexpr int kMinBlocks = RHP_MIN_BLOCKS;  // resident CTAs per SM the SpMV is built for
+// The thread-per-row kernel is built for 4 resident CTAs per SM (64
+// registers; its never-taken merge-path copy spills, its row loop does not
+// need more): one row in flight per thread is hidden by occupancy. C4 K2
+// 602 -> 450 us (0.97 of the HBM roofline), C3 K2 21.5 -> 18.9 us; 3 CTAs:
+// 520 us; the rows-only kernel at 4 CTAs: 537 us (A/B on one box).
+#ifndef RHP_ROWS_MIN_BLOCKS
+#define RHP_ROWS_MIN_BLOCKS 4
+#endif
+constexpr int kRowsMinBlocks = RHP_ROWS_MIN_BLOCKS;  // ... and the thread-per-row kernel
 constexpr int kPer = RHP_WIN_PER;           // nonzeros per lane per window
 constexpr int kWin = 32 * kPer;             // nonzeros per warp window
 static_assert(kPer == 4 || kPer == 8 || kPer == 16, "window of 4, 8 or 16 nonzeros per lane");
@@ -145,6 +154,9 @@ constexpr int kCtaRowBlocks = RHP_CTA_BLOCKS;  // resident CTAs per SM the kerne
 #endif
 #ifndef RHP_ROWS_KERNEL_COMBINED
 #define RHP_ROWS_KERNEL_COMBINED 1  // spmv_rows also carries the merge path (spmv.cuh)
+#endif
+#ifndef RHP_ROWS_VEC
+#define RHP_ROWS_VEC 1  // thread-per-row, uniform rows of a multiple of 4: 16-B index/value loads
 #endif
 #ifndef RHP_UNIFORM_RF
 #define RHP_UNIFORM_RF 1  // rows in flight of the thread-per-row engine on uniform rows

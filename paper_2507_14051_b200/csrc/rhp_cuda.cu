@@ -442,6 +442,19 @@ void launch_spmv(rhp_ctx& c, const DevOp& op, int grid, const double* xg, const 
   launch_one(c, op.segs.back(), grid, xg, epi, part, ticket, s);
 }
 
+// Resident CTAs per SM of the thread-per-row kernel of an epilogue.
+template <class Epi>
+int prepare_rows() {
+  int b = 0, b1 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b, reinterpret_cast<const void*>(spmv_rows<Epi, false>), kBlock, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &b1, reinterpret_cast<const void*>(spmv_rows<Epi, true>), kBlock, 0));
+  b = std::min(b, b1);
+  if (b < 1) throw CudaError("spmv kernel does not fit on an SM");
+  return b;
+}
+
 // Resident CTAs per SM of an SpMV instantiation.
 template <class Epi>
 int prepare_spmv() {
@@ -538,7 +551,7 @@ __global__ void __launch_bounds__(256) k_gather_probe(const int32_t* __restrict_
 // contexts on one LP always agree bit for bit): thread-per-row when the
 // longest row has <= kThreadRowMax nonzeros, else the merge-path warp engine.
 // RHP_THREAD_ROWS=0 forces merge path; =1 allows rows up to 64 nonzeros.
-void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
+bool thread_rows_rule(const std::vector<int64_t>& rp, int64_t* longest_out = nullptr) {
   // RHP_THREAD_ROWS: 0 forces the merge path, 1 allows rows up to 64, a
   // larger number is the cap itself (A/B runs)
   const char* env = std::getenv("RHP_THREAD_ROWS");
@@ -550,7 +563,14 @@ void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
   const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
   int64_t longest = 0;
   for (int64_t r = 0; r < rows; ++r) longest = std::max(longest, rp[r + 1] - rp[r]);
-  if (rows > 0 && longest <= cap) {
+  if (longest_out) *longest_out = longest;
+  return rows > 0 && longest <= cap;
+}
+
+void apply_engine_rule(DevOp& d, const std::vector<int64_t>& rp) {
+  const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
+  int64_t longest = 0;
+  if (thread_rows_rule(rp, &longest)) {
     d.sched.thread_rows = 1;
     d.sched.n_multi = 0;  // no split rows: K1's finalize reads no slots of this operator
     // every row of one length: row starts are arithmetic (RHP_UNIFORM=0 off)
@@ -1535,8 +1555,15 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     const int occ_store = prepare_spmv<EpiStore>();
     const int occ_a = std::min({prepare_spmv<EpiDual>(), prepare_spmv<EpiKktRow>(),
                                 prepare_spmv<EpiKktRowDist>(), occ_store});
-    const int occ_at = std::min({prepare_spmv<EpiAty>(), prepare_spmv<EpiKktCol>(),
-                                 prepare_spmv<EpiPowerW>(), occ_store});
+    int occ_at = std::min({prepare_spmv<EpiAty>(), prepare_spmv<EpiKktCol>(),
+                           prepare_spmv<EpiPowerW>(), occ_store});
+    // A^T walked by the thread-per-row engine only (single GPU: its walkers
+    // are spmv_rows and K3's epilogue_walk, grid-stride loops over the same
+    // thread map): the grid follows the rows kernel's own register budget
+    // (RHP_ROWS_MIN_BLOCKS)
+    if (!c->dist && kRowsMinBlocks > kMinBlocks && thread_rows_rule(c->L.At.rp))
+      occ_at = std::min({prepare_rows<EpiAty>(), prepare_rows<EpiKktCol>(), prepare_rows<EpiPowerW>(),
+                         prepare_rows<EpiStore>()});
     // at least ~2 windows of work per warp, at most every resident CTA
     auto clampg = [](const HostOperator& h, int64_t cap) {
       const int64_t work = h.nnz + 2 * h.rows;

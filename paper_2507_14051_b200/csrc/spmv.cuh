@@ -373,17 +373,30 @@ __device__ __forceinline__ void thread_rows(const int32_t* ci, const double* val
         }
         lmax = max(lmax, len[f]);
       }
+      // uniform rows of a multiple of 4 in CSR order: a row's 4 elements of
+      // one step are 16-B aligned (i * w), one int4 + two double2 loads
+      const bool vec = RHP_ROWS_VEC && EC == 4 && w > 0 && (w & 3) == 0 && !sliced;
       for (int t = 0; t < lmax; t += EC) {
         int c[RF][EC];
         double v[RF][EC], g[RF][EC];
 #pragma unroll
-        for (int f = 0; f < RF; ++f)
+        for (int f = 0; f < RF; ++f) {
+          if (vec) {
+            const bool ok = t < len[f];
+            const int4 q = ok ? __ldcs(reinterpret_cast<const int4*>(cix + lo[f] + t)) : make_int4(0, 0, 0, 0);
+            const double2 a = ok ? __ldcs(reinterpret_cast<const double2*>(vx + lo[f] + t)) : make_double2(0.0, 0.0);
+            const double2 b = ok ? __ldcs(reinterpret_cast<const double2*>(vx + lo[f] + t) + 1) : make_double2(0.0, 0.0);
+            c[f][0] = q.x; c[f][1] = q.y; c[f][2] = q.z; c[f][3] = q.w;
+            v[f][0] = a.x; v[f][1] = a.y; v[f][2] = b.x; v[f][3] = b.y;
+            continue;
+          }
 #pragma unroll
           for (int u = 0; u < EC; ++u) {
             const bool ok = t + u < len[f];
             c[f][u] = ok ? __ldcs(cix + lo[f] + (t + u) * es) : 0;
             v[f][u] = ok ? __ldcs(vx + lo[f] + (t + u) * es) : 0.0;
           }
+        }
 #pragma unroll
         for (int f = 0; f < RF; ++f)
 #pragma unroll
@@ -454,7 +467,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
 // shared-memory carveout preference (25-100 %: C4 K2 1.29 ms) — kept for
 // the measured speed.
 template <class Epi, bool L1G = false>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_rows(Csr A, const double* __restrict__ xg,
+__global__ void __launch_bounds__(kBlock, kRowsMinBlocks) spmv_rows(Csr A, const double* __restrict__ xg,
                                                                 Sched s, Epi epi, double* part,
                                                                 unsigned int* ticket) {
   pdl_wait();

@@ -1553,8 +1553,10 @@ int rhp_create(const rhpdhg_lp_view* lp, const rhp_options* opt_in, rhp_ctx** ou
     // grids: persistent, a multiple of the SM count, never more than tiles
     // one grid per operator: every kernel walking it must see the same CTA count
     const int occ_store = prepare_spmv<EpiStore>();
-    const int occ_a = std::min({prepare_spmv<EpiDual>(), prepare_spmv<EpiKktRow>(),
-                                prepare_spmv<EpiKktRowDist>(), occ_store});
+    int occ_a = std::min({prepare_spmv<EpiDual>(), prepare_spmv<EpiKktRow>(),
+                          prepare_spmv<EpiKktRowDist>(), occ_store});
+    if (!c->dist && kRowsMinBlocks > kMinBlocks && thread_rows_rule(c->L.A.rp))
+      occ_a = std::min({prepare_rows<EpiDual>(), prepare_rows<EpiKktRow>(), prepare_rows<EpiStore>()});
     int occ_at = std::min({prepare_spmv<EpiAty>(), prepare_spmv<EpiKktCol>(),
                            prepare_spmv<EpiPowerW>(), occ_store});
     // A^T walked by the thread-per-row engine only (single GPU: its walkers

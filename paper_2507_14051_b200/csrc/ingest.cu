@@ -22,7 +22,9 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -361,7 +363,14 @@ bool maybe_relabel(DeviceCsr& A, DeviceCsr& At, int64_t m, int64_t n, int locali
   ICK(cudaGetLastError());
   int passes = kRelabelPasses;
   if (const char* e = std::getenv("RHP_RELABEL_PASSES")) passes = std::max(1, std::atoi(e));
+  const bool trace = std::getenv("RHPDHG_SETUP_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
   for (int p = 0; p < passes; ++p) relabel_pass(A, At, m, n, ordr.p, ordc.p, s);
+  if (trace) {
+    ICK(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "    relabel %d passes %9.3f s\n", passes,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
   const double sa = static_cast<double>(window_sectors(A, s)), st = static_cast<double>(window_sectors(At, s));
   sectors[2] = sa / static_cast<double>(nnz);
   sectors[3] = st / static_cast<double>(nnz);

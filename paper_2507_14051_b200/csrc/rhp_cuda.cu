@@ -15,6 +15,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -343,6 +344,22 @@ int64_t contiguous_start(const std::vector<int32_t>& perm) {
   return perm.empty() ? 0 : perm[0];
 }
 
+// Host loop over [0, n) split across the host's threads (the order maps of a
+// relabelled layout touch tens of millions of entries per vector copy).
+template <class F>
+void host_parallel_for(size_t n, F&& f) {
+  const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t T = std::min<size_t>(std::min<size_t>(hw, 16), n / (1u << 20) + 1);
+  if (T <= 1) {
+    f(size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (size_t t = 0; t < T; ++t) th.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T); });
+  for (auto& x : th) x.join();
+}
+
 // gather a host vector in original order into device order
 void upload_perm(double* dst, const double* src, const std::vector<int32_t>& perm,
                  std::vector<double>& scratch, cudaStream_t s) {
@@ -353,7 +370,9 @@ void upload_perm(double* dst, const double* src, const std::vector<int32_t>& per
     return;
   }
   scratch.resize(perm.size());
-  for (size_t i = 0; i < perm.size(); ++i) scratch[i] = src[perm[i]];
+  host_parallel_for(perm.size(), [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) scratch[i] = src[perm[i]];
+  });
   upload(dst, scratch.data(), scratch.size(), s);
   CK(cudaStreamSynchronize(s));  // scratch is reused
 }
@@ -372,7 +391,9 @@ void download_perm(double* dst, const double* src_dev, const std::vector<int32_t
     CK(cudaMemcpyAsync(scratch.data(), src_dev, perm.size() * sizeof(double),
                        cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  for (size_t i = 0; i < perm.size(); ++i) dst[perm[i]] = scratch[i];
+  host_parallel_for(perm.size(), [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) dst[perm[i]] = scratch[i];
+  });
 }
 
 // perm for local rows: prow holds global row ids; make them local

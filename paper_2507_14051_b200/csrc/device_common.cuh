@@ -135,7 +135,7 @@ constexpr int64_t kThreadRowMax = 8;
 // engine (spmv.cuh spmv_cta_rows), kCtaRowsBatch rows per CTA pass.
 constexpr int64_t kCtaRowMin = 256;
 #ifndef RHP_CTA_BATCH
-#define RHP_CTA_BATCH 2
+#define RHP_CTA_BATCH 4
 #endif
 #ifndef RHP_CTA_UNROLL
 #define RHP_CTA_UNROLL 4

@@ -185,6 +185,7 @@ void build_transpose(const DeviceCsr& A, int64_t n, DeviceCsr& At, cudaStream_t 
 
 constexpr double kRelabelGain = 0.8;  // keep when sectors(new) <= 0.8 * sectors(old)
 constexpr int kRelabelPasses = 2;
+constexpr double kRelabelSkip = 0.95;  // sectors per nonzero of an already scattered operator
 
 // key[j] = first row touching column j (A^T rows ascend), empty: UINT32_MAX
 __global__ void k_col_first(const int64_t* trp, const int32_t* tci, int64_t n, uint32_t* key) {
@@ -342,6 +343,10 @@ bool maybe_relabel(DeviceCsr& A, DeviceCsr& At, int64_t m, int64_t n, int locali
   const double before = sa0 + st0;
   sectors[0] = sa0 / static_cast<double>(A.nnz);
   sectors[1] = st0 / static_cast<double>(A.nnz);
+  // every gather already on a sector of its own (uniformly scattered
+  // columns, C5): first touch has nothing to regroup (C2-like LPs gain ~10 %
+  // at best, below kRelabelGain) — skip the passes (C5: ~10 s of setup)
+  if (locality == 0 && sectors[0] > kRelabelSkip && sectors[1] > kRelabelSkip) return false;
   // keep A's original arrays until the verdict (A^T is rebuilt from them on
   // a revert); skipped in auto mode when the device cannot hold the copies
   // and the sort buffers (~60 B per nonzero)

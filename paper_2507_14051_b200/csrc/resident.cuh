@@ -32,7 +32,7 @@
 namespace rhp {
 
 #ifndef RHP_RES_THREADS
-#define RHP_RES_THREADS 256
+#define RHP_RES_THREADS 512  // C1: 122k (256) -> 125k iter/s; 1024 exceeds shared memory
 #endif
 constexpr int kResThreads = RHP_RES_THREADS;
 constexpr int kResWarps = kResThreads / 32;

@@ -937,16 +937,23 @@ void build_segments(rhp_ctx& c, DevOp& d, const HostOperator& h, int64_t cols, i
   }
 }
 
-// Gather cache policy (ld_gather): L1::no_allocate by default; RHP_L1_GATHER=1
-// selects the L1-allocating variant. A timing-based choice per operator was
-// used while the gathers had the default L2 policy (C4 gained 17 % from L1);
-// with evict_last gathers L1 no longer wins anywhere (C2 6958 vs 6620, C3
-// 22.9k both, C4 1102 vs 1076 iter/s), so the policy is fixed and
-// deterministic. The policy never changes a result.
+// Gather cache policy (ld_gather): L1::no_allocate, except A's gathers on a
+// relabelled layout, which allocate in L1 (first-touch order puts a row's
+// columns side by side, so neighbouring lanes and the next window re-read
+// the lines: C4 K1 596 -> 586 us, 912 -> 929 iter/s, A/B twice on one box;
+// Aᵀ neutral). Without relabelling L1 wins nowhere (C2 6958 vs 6620, C3
+// 22.9k both, C4 1102 vs 1076 iter/s in round 1). RHP_L1_GATHER overrides:
+// 0 none, 1 both operators, A / T one of them. Deterministic, and the policy
+// never changes a result.
 void choose_gather_policy(rhp_ctx& c) {
-  const char* env = std::getenv("RHP_L1_GATHER");  // 1: both operators, A / T: one of them
-  c.A.l1g = env && (env[0] == '1' || env[0] == 'A');
-  c.At.l1g = env && (env[0] == '1' || env[0] == 'T');
+  const char* env = std::getenv("RHP_L1_GATHER");
+  if (!env) {
+    c.A.l1g = c.L.relabel;
+    c.At.l1g = false;
+    return;
+  }
+  c.A.l1g = env[0] == '1' || env[0] == 'A';
+  c.At.l1g = env[0] == '1' || env[0] == 'T';
 }
 
 // Peer-memory exchange (peer.cuh): one cudaMalloc'd region per rank, its

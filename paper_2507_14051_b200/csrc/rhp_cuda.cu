@@ -1836,8 +1836,11 @@ int rhp_get_scaled(rhp_ctx* c, const rhp_scaled_out* o) {
   return guarded([&] {
     const HostLayout& L = c->L;
     const std::vector<int32_t> lrows = local_rows(*c);
-    // device element order = the reference's CSR / CSC order
+    // device element order = the reference's CSR / CSC order (not on a
+    // relabelled layout: the matrix values are only available unrelabelled)
     const size_t nz = static_cast<size_t>(L.nnz);
+    if ((o->csr_values || o->csc_values) && nz && c->L.relabel)
+      throw std::invalid_argument("rhp_get_scaled: matrix values of a relabelled layout");
     if (o->csr_values && nz) CK(cudaMemcpy(o->csr_values, c->A.v, nz * sizeof(double), cudaMemcpyDeviceToHost));
     if (o->csc_values && nz) CK(cudaMemcpy(o->csc_values, c->At.v, nz * sizeof(double), cudaMemcpyDeviceToHost));
     if (o->row_scale) download_perm(o->row_scale, c->rs, lrows, c->hbuf, c->stream);
@@ -2304,8 +2307,8 @@ int rhp_set_vectors(rhp_ctx* c, const rhp_op_lp* lp) {
 
 int rhp_set_csc_values(rhp_ctx* c, const double* csc_values, int scale_source) {
   return guarded([&] {
-    if (c->scaled || c->dist)
-      throw std::invalid_argument("rhp_set_csc_values: needs an unscaled single-GPU context");
+    if (c->scaled || c->dist || c->L.relabel)
+      throw std::invalid_argument("rhp_set_csc_values: needs an unscaled, unrelabelled single-GPU context");
     const size_t nz = static_cast<size_t>(c->L.nnz);
     if (!nz) return;
     if (scale_source) {

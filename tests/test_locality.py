@@ -104,3 +104,12 @@ def test_relabelled_first_iterates(gpu):
     finally:
         set_locality(0)
         set_resident(-1)
+
+
+def test_matrix_values_of_a_relabelled_layout_are_refused(gpu):
+    """The per-op API's CSR/CSC value exchange is in the reference's element
+    order, which only an unrelabelled layout has: refused, not reordered."""
+    with DeviceContext(LPS[0], locality=1) as dev:
+        dev.scale()
+        with pytest.raises(Exception, match="relabelled"):
+            dev.get_scaled()

@@ -459,13 +459,15 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) spmv_fused(Csr A, const do
   spmv_tail(s, epi, acc, part, ticket);
 }
 
-// Thread-per-row operators (Sched::thread_rows) launch this one; same grid
-// and epilogue contract as spmv_fused. It still carries the merge path
+// Thread-per-row operators (Sched::thread_rows) launch this one; same
+// epilogue contract as spmv_fused, built for kRowsMinBlocks (4) CTAs per SM
+// with the operator's grid sized for it (rhp_cuda.cu thread_rows_rule; C4
+// K2 602 -> 450 us). It still carries the merge path
 // (RHP_ROWS_KERNEL_COMBINED, never taken at run time): the thread-per-row
-// code nvcc emits without it is slower (C4 K2 619 vs 565 us, C3 24.4 vs
-// 20.9 us, A/B on one box), and so is the rows-only kernel under a
-// shared-memory carveout preference (25-100 %: C4 K2 1.29 ms) — kept for
-// the measured speed.
+// code nvcc emits without it is slower (C4 K2 537 vs 450 us at 4 CTAs/SM,
+// 619 vs 565 us at 2), and so is the rows-only kernel under a shared-memory
+// carveout preference (25-100 %: C4 K2 1.29 ms) — kept for the measured
+// speed.
 template <class Epi, bool L1G = false>
 __global__ void __launch_bounds__(kBlock, kRowsMinBlocks) spmv_rows(Csr A, const double* __restrict__ xg,
                                                                 Sched s, Epi epi, double* part,
